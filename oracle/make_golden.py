@@ -1,0 +1,306 @@
+"""Generate tests/golden/*.npz by running the REAL reference (voxtop) here.
+
+TEST INFRASTRUCTURE ONLY.  Run in the build container, where
+/root/reference exists:
+
+    python oracle/make_golden.py [--skip-traj]
+
+The fixtures pin both the oracle restatement (tests/test_oracle_golden.py,
+CPU) and the CUDA path (tests/test_gpu_*.py).  /root/reference does not exist
+on the GPU box, so nothing but these committed files travels.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+def _vt():
+    sys.path.insert(0, REF)
+    import voxtop as vt  # noqa: E402
+
+    return vt
+
+
+def face_mask(vt, grid, axis=0, side=0):
+    mask = np.zeros(grid.n_dofs, dtype=bool)
+    rng_ = [range(grid.nelx + 1), range(grid.nely + 1), range(grid.nelz + 1)]
+    rng_[axis] = [0 if side == 0 else rng_[axis][-1]]
+    for k in rng_[2]:
+        for j in rng_[1]:
+            for i in rng_[0]:
+                nd = grid.node_id(i, j, k)
+                mask[3 * nd : 3 * nd + 3] = True
+    return mask
+
+
+def gen_k0(vt):
+    out = {}
+    for tag, nu, h in (("a", 0.3, 1.0), ("b", 0.3, 4.0 / 3.0), ("c", 0.2, 0.25), ("d", 0.45, 2.0)):
+        out[f"k0_{tag}"] = vt.unit_stiffness(nu, h).matrix
+        out[f"nu_{tag}"] = nu
+        out[f"h_{tag}"] = h
+    np.savez_compressed(os.path.join(OUT, "k0.npz"), **out)
+
+
+def gen_operator(vt):
+    rng = np.random.default_rng(20261017)
+    out = {}
+    cases = [(2, 1, 1), (3, 2, 2), (6, 6, 6), (5, 4, 3), (9, 7, 5), (33, 17, 9)]
+    for ci, dims in enumerate(cases):
+        h = [1.0, 0.5, 1.25][ci % 3]
+        grid = vt.build_grid(*dims, h)
+        rho = rng.uniform(0.0, 1.0, grid.n_elements)
+        fixed = rng.choice(grid.n_dofs, size=grid.n_dofs // 10 + 3, replace=False)
+        st = vt.OperatorState(grid, rho, vt.MaterialModel(), fixed, vt.unit_stiffness(0.3, h))
+        u = rng.standard_normal(grid.n_dofs)
+        f = rng.standard_normal(grid.n_dofs)
+        out[f"c{ci}_dims"] = np.array(dims)
+        out[f"c{ci}_h"] = h
+        out[f"c{ci}_rho"] = rho
+        out[f"c{ci}_fixed"] = np.sort(fixed)
+        out[f"c{ci}_u"] = u
+        out[f"c{ci}_f"] = f
+        out[f"c{ci}_scale"] = st.scale
+        out[f"c{ci}_v"] = vt.apply(st, u)
+        out[f"c{ci}_d"] = vt.diagonal(st)
+        out[f"c{ci}_r"] = vt.residual(st, u, f)
+    out["ncases"] = len(cases)
+    np.savez_compressed(os.path.join(OUT, "operator.npz"), **out)
+
+
+def gen_multigrid(vt):
+    rng = np.random.default_rng(77)
+    out = {}
+    # transfers + per-level data on an 8x4x4 grid, 3 levels
+    for tag, dims, L in (("t", (8, 4, 4), 3), ("v", (16, 8, 8), 3), ("w", (24, 12, 12), 3)):
+        grid = vt.build_grid(*dims, 1.0)
+        rho = rng.uniform(0.05, 1.0, grid.n_elements)
+        st = vt.OperatorState(grid, rho, vt.MaterialModel(), face_mask(vt, grid))
+        hier = vt.build_hierarchy(grid, st, L, scheme="homogenized")
+        out[f"{tag}_dims"] = np.array(dims)
+        out[f"{tag}_rho"] = rho
+        out[f"{tag}_levels"] = hier.n_levels
+        for l, lv in enumerate(hier.levels):
+            out[f"{tag}_scale{l}"] = lv.scale
+            out[f"{tag}_diag{l}"] = lv.diag
+            out[f"{tag}_fixed{l}"] = lv.fixed_idx
+        for l in range(hier.n_levels - 1):
+            rf = rng.standard_normal(hier.levels[l].n_dofs)
+            ec = rng.standard_normal(hier.levels[l + 1].n_dofs)
+            out[f"{tag}_rf{l}"] = rf
+            out[f"{tag}_rc{l}"] = hier.restrict(l, rf)
+            out[f"{tag}_ec{l}"] = ec
+            out[f"{tag}_ef{l}"] = hier.prolongate(l, ec)
+        for l in range(1, hier.n_levels):
+            uc = rng.standard_normal(hier.levels[l].n_dofs)
+            out[f"{tag}_cu{l}"] = uc
+            out[f"{tag}_cv{l}"] = hier.coarse_apply(l, uc)
+        f = rng.standard_normal(grid.n_dofs)
+        f[st.fixed_idx] = 0.0
+        u = rng.standard_normal(grid.n_dofs)
+        out[f"{tag}_f"] = f
+        out[f"{tag}_z"] = hier.v_cycle(f)
+        out[f"{tag}_ju"] = u
+        out[f"{tag}_js"] = hier.jacobi_smooth(0, u, f, 2)
+        fL = rng.standard_normal(hier.levels[-1].n_dofs)
+        fL[hier.levels[-1].fixed_idx] = 0.0
+        out[f"{tag}_fL"] = fL
+        out[f"{tag}_uL"] = hier.coarse_solve(fL)
+        out[f"{tag}_vector_scalars"] = hier.vector_scalars
+        out[f"{tag}_operator_scalars"] = hier.operator_scalars
+        out[f"{tag}_factor_scalars"] = hier.factor_scalars
+    np.savez_compressed(os.path.join(OUT, "multigrid.npz"), **out)
+
+
+def gen_pcg(vt):
+    from voxtop.app.presets import instantiate
+    from voxtop.solver import jacobi_preconditioner
+
+    out = {}
+    rng = np.random.default_rng(5)
+    problem, _ = instantiate("cantilever", (16, 8, 8))
+    grid = problem.grid
+    fm = problem.boundary.fixed_mask(grid)
+    f = problem.boundary.external_force(grid)
+    f[np.flatnonzero(fm)] = 0.0
+    for tag, rho in (("u", np.full(grid.n_elements, 0.12)), ("r", rng.uniform(0.01, 1.0, grid.n_elements))):
+        st = vt.OperatorState(grid, rho, problem.model, fm, problem.stiffness())
+        hier = vt.build_hierarchy(grid, st, 3, scheme="homogenized")
+        for ctag, cfg, u0 in (
+            ("a", vt.SolverConfig(tolerance=1e-5), None),
+            ("b", vt.SolverConfig(tolerance=1e-10, max_iterations=500), None),
+            ("c", vt.SolverConfig(tolerance=1e-12, max_iterations=3), None),
+            ("d", vt.SolverConfig(tolerance=1e-8, max_iterations=120), "warm"),
+        ):
+            u_init = None
+            if u0 == "warm":
+                u_init = rng.standard_normal(grid.n_dofs) * 1e-3
+                out[f"{tag}{ctag}_u0"] = u_init
+            x, rep = vt.mgcg_solve(st, hier, f, u_prev=u_init, cfg=cfg)
+            out[f"{tag}{ctag}_x"] = x
+            out[f"{tag}{ctag}_rep"] = np.array(
+                [rep.iterations, rep.final_rel_residual, rep.precond_applications,
+                 float(rep.converged), rep.aux_vector_scalars, rep.residual_drift]
+            )
+        out[f"{tag}_rho"] = rho
+        cfg = vt.SolverConfig(tolerance=1e-8, max_iterations=2000)
+        x, rep = vt.pcg(st, jacobi_preconditioner(st), f, cfg=cfg)
+        out[f"{tag}j_x"] = x
+        out[f"{tag}j_rep"] = np.array([rep.iterations, rep.final_rel_residual, rep.precond_applications, float(rep.converged)])
+        x, rep = vt.pcg(st, None, f, cfg=cfg)
+        out[f"{tag}n_x"] = x
+        out[f"{tag}n_rep"] = np.array([rep.iterations, rep.final_rel_residual, rep.precond_applications, float(rep.converged)])
+    out["f"] = f
+    np.savez_compressed(os.path.join(OUT, "pcg.npz"), **out)
+
+
+def gen_design(vt):
+    from voxtop.optimize import DensityField
+
+    rng = np.random.default_rng(11)
+    out = {}
+    grid = vt.build_grid(12, 6, 5, 0.75)
+    rho = rng.uniform(0.02, 1.0, grid.n_elements)
+    st = vt.OperatorState(grid, rho, vt.MaterialModel(), face_mask(vt, grid), vt.unit_stiffness(0.3, 0.75))
+    u = rng.standard_normal(grid.n_dofs)
+    grav = vt.GravitySpec(axis=2, g=9.81, unit_weight=0.7)
+    out["rho"] = rho
+    out["u"] = u
+    out["dc"] = vt.sensitivities(st, u)
+    out["dcg"] = vt.sensitivities(st, u, grav)
+    regions = vt.classify_regions(grid, [])
+    f_ext = np.zeros(grid.n_dofs)
+    f_ext[rng.choice(grid.n_dofs, 20, replace=False)] = rng.standard_normal(20)
+    out["f_ext"] = f_ext
+    out["fgrav"] = vt.update_gravity_load(grid, DensityField(rho, regions), grav, f_ext, st.fixed_idx)
+    out["fgrav_plain"] = vt.update_gravity_load(grid, DensityField(rho, regions), grav)
+    dc = -rng.uniform(0.1, 5.0, grid.n_elements)
+    out["dcin"] = dc
+    for tag, r in (("r15", 1.5 * 0.75), ("r25", 2.5 * 0.75), ("r18", 1.8 * 0.75)):
+        w = vt.build_filter(grid, r)
+        out[f"{tag}_kernel"] = w.kernel
+        out[f"{tag}_wsum"] = w.wsum
+        out[f"{tag}_dcf"] = vt.filter_sensitivities(dc, rho, w, 1e-3)
+    # OC on an instance with passives
+    boxes = [(vt.Box((0, 0, 0), (0.75, 4.5, 3.75)), vt.Region.PASSIVE_SOLID),
+             (vt.Box((8.25, 0, 0), (9.0, 4.5, 3.75)), vt.Region.PASSIVE_VOID)]
+    reg = vt.classify_regions(grid, boxes)
+    from voxtop.optimize import initial_densities
+
+    x0 = initial_densities(reg, 0.3).values.copy()
+    x0[reg.active] = rng.uniform(0.05, 0.6, reg.n_active)
+    x0[reg.active] += 0.3 - x0[reg.active].mean()
+    x0 = np.clip(x0, 0, 1)
+    out["oc_x0"] = x0
+    out["oc_classes"] = reg.classes
+    for tag, kw in (("a", dict(volfrac=0.3)), ("b", dict(volfrac=0.3, move=0.1, q=2.0)), ("c", dict(volfrac=0.25, eta=0.3))):
+        cfg = vt.OptConfig(filter_radius=1.0, **kw)
+        res = vt.oc_update(DensityField(x0, reg), dc, np.ones(grid.n_elements), cfg)
+        out[f"oc{tag}_rho"] = res.densities.values
+        out[f"oc{tag}_lam"] = res.lam
+        out[f"oc{tag}_steps"] = res.bisection_steps
+    np.savez_compressed(os.path.join(OUT, "design.npz"), **out)
+
+
+def _traj(vt, problem, opt, iters_keep, scheme="homogenized", max_levels=None, keep_u=False):
+    recs, snaps = [], {}
+
+    def hook(rec, rho, u):
+        recs.append([rec.iteration, rec.compliance, rec.volume, rec.change, rec.cg_iters,
+                     rec.cg_residual, rec.aux_scalars])
+        if rec.iteration in iters_keep:
+            snaps[f"rho{rec.iteration}"] = rho.values.copy()
+            if keep_u:
+                snaps[f"u{rec.iteration}"] = u.copy()
+
+    t0 = time.perf_counter()
+    res = vt.run(problem, opt, vt.SolverConfig(tolerance=1e-5), scheme=scheme,
+                 max_levels=max_levels, on_iteration=hook)
+    return np.array(recs), snaps, time.perf_counter() - t0, res
+
+
+def gen_traj(vt, which):
+    from voxtop.app.presets import instantiate
+    from voxtop.app import presets as P
+    from voxtop.errors import VolumeInfeasible
+
+    if "cfg1" in which:
+        problem, _ = instantiate("cantilever", (48, 24, 24))
+        h = problem.grid.h
+        opt = vt.OptConfig(volfrac=0.12, filter_radius=1.5 * h, p=3.0, max_iterations=40, ch_tol=1e-12)
+        recs, snaps, wall, _ = _traj(vt, problem, opt, {1, 5, 10, 20, 40}, max_levels=4, keep_u=False)
+        np.savez_compressed(os.path.join(OUT, "cfg1_traj.npz"), recs=recs, wall=wall, **snaps)
+        print("cfg1", wall, recs[:, 4])
+    if "small" in which:
+        # fast end-to-end trajectory for GPU parity (16x8x8 cantilever, 2.5h filter)
+        problem, _ = instantiate("cantilever", (16, 8, 8))
+        h = problem.grid.h
+        opt = vt.OptConfig(volfrac=0.12, filter_radius=2.5 * h, max_iterations=30, ch_tol=1e-12)
+        recs, snaps, wall, _ = _traj(vt, problem, opt, {1, 10, 30}, max_levels=3, keep_u=True)
+        np.savez_compressed(os.path.join(OUT, "small_traj.npz"), recs=recs, **snaps)
+    if "bridge" in which:
+        grid = vt.build_grid(32, 16, 16, 2.0)
+        fixed = P._fix_all(grid, P._bottom_corner_nodes(grid))
+        loads = P._face_pressure_loads(grid, 2, 1, 2, -100.0)
+        bnd = vt.make_boundary(grid, fixed, loads)
+        Lx, Ly, Lz = grid.domain
+        reg = vt.classify_regions(grid, [(vt.Box((0, 0, Lz - grid.h), (Lx, Ly, Lz)), vt.Region.PASSIVE_SOLID)])
+        problem = vt.Problem(grid, bnd, reg)
+        opt = vt.OptConfig(volfrac=0.14, filter_radius=1.5 * grid.h, max_iterations=3, ch_tol=1e-12)
+        recs, snaps, wall, _ = _traj(vt, problem, opt, {3})
+        np.savez_compressed(os.path.join(OUT, "bridge_traj.npz"), recs=recs, **snaps)
+    if "grav" in which:
+        problem, _ = instantiate("cantilever", (32, 16, 16))
+        grid = problem.grid
+        bnd = problem.boundary
+        gb = vt.BoundarySpec(bnd.fixed_dofs, bnd.load_dofs, bnd.load_values,
+                             vt.GravitySpec(axis=2, g=1.0, unit_weight=1e-3))
+        p2 = vt.Problem(grid, gb, problem.regions)
+        opt = vt.OptConfig(volfrac=0.12, filter_radius=1.5 * grid.h, max_iterations=4, ch_tol=1e-12)
+        recs, snaps, wall, _ = _traj(vt, p2, opt, {4})
+        np.savez_compressed(os.path.join(OUT, "grav_traj.npz"), recs=recs, **snaps)
+        gb = vt.BoundarySpec(bnd.fixed_dofs, bnd.load_dofs, bnd.load_values,
+                             vt.GravitySpec(axis=2, g=1.0, unit_weight=1.0))
+        p3 = vt.Problem(grid, gb, problem.regions)
+        seen = []
+        info = {}
+        try:
+            vt.run(p3, opt, vt.SolverConfig(tolerance=1e-5), scheme="homogenized",
+                   on_iteration=lambda r, a, b: seen.append(r.compliance))
+            info["raised"] = None
+        except VolumeInfeasible as exc:
+            info["raised"] = "VolumeInfeasible"
+            info["msg"] = str(exc)
+        info["compliance"] = seen
+        with open(os.path.join(OUT, "grav_fail.json"), "w") as fh:
+            json.dump(info, fh, indent=1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="k0,operator,multigrid,pcg,design,small,bridge,grav,cfg1")
+    a = ap.parse_args()
+    os.makedirs(OUT, exist_ok=True)
+    vt = _vt()
+    which = set(a.only.split(","))
+    for name, fn in (("k0", gen_k0), ("operator", gen_operator), ("multigrid", gen_multigrid),
+                     ("pcg", gen_pcg), ("design", gen_design)):
+        if name in which:
+            t = time.perf_counter()
+            fn(vt)
+            print(name, f"{time.perf_counter() - t:.1f}s")
+    gen_traj(vt, which)
+
+
+if __name__ == "__main__":
+    main()

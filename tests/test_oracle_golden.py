@@ -1,0 +1,198 @@
+"""Pin the CPU oracle (oracle/cpu_path.py) to the real reference's outputs.
+
+The fixtures under tests/golden were produced by oracle/make_golden.py from
+/root/reference (voxtop 0.1.0).  Deterministic numpy pipelines are expected
+to agree bit for bit; BLAS/LAPACK-dependent ones (dgemm, ddot, Cholesky) to
+within a few ulps.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, face_fixed_mask, golden, rel_err
+from oracle import cpu_path as O
+
+
+def test_k0_closed_form():
+    g = golden("k0.npz")
+    for t in "abcd":
+        k = O.hex8_k0(float(g[f"nu_{t}"]), float(g[f"h_{t}"]))
+        assert np.array_equal(k, g[f"k0_{t}"])
+
+
+def test_k0_constant_diagonal():
+    k = O.hex8_k0(0.3, 1.0)
+    assert np.unique(np.diag(k)).size == 1
+
+
+def _op_case(g, ci):
+    dims = tuple(int(x) for x in g[f"c{ci}_dims"])
+    es = (dims[2], dims[1], dims[0])
+    h = float(g[f"c{ci}_h"])
+    return dims, es, h
+
+
+def test_operator_apply_diag_residual():
+    g = golden("operator.npz")
+    for ci in range(int(g["ncases"])):
+        dims, es, h = _op_case(g, ci)
+        k0 = O.hex8_k0(0.3, h)
+        scale = 1.0 * O.simp(g[f"c{ci}_rho"], 3.0, 1e-9)
+        assert np.array_equal(scale, g[f"c{ci}_scale"])
+        fx = g[f"c{ci}_fixed"]
+        v = O.apply_k(g[f"c{ci}_u"], es, fx, k0, scale)
+        assert np.array_equal(v, g[f"c{ci}_v"])
+        d = O.diag_k(es, fx, k0, scale)
+        assert np.array_equal(d, g[f"c{ci}_d"])
+        r = O.resid_k(g[f"c{ci}_u"], g[f"c{ci}_f"], es, fx, k0, scale)
+        assert np.array_equal(r, g[f"c{ci}_r"])
+
+
+def test_dense_oracle_consistency():
+    g = golden("operator.npz")
+    for ci in range(3):
+        dims, es, h = _op_case(g, ci)
+        k0 = O.hex8_k0(0.3, h)
+        K = O.dense_k(es, g[f"c{ci}_fixed"], k0, g[f"c{ci}_scale"])
+        assert rel_err(K @ g[f"c{ci}_u"], g[f"c{ci}_v"]) <= 1e-12
+
+
+def _hier(g, tag):
+    dims = tuple(int(x) for x in g[f"{tag}_dims"])
+    es = (dims[2], dims[1], dims[0])
+    mask = face_fixed_mask(*dims)
+    rho = g[f"{tag}_rho"]
+    H = O.hier_build(es, 1.0, mask, int(g[f"{tag}_levels"]))
+    k0 = O.hex8_k0(0.3, 1.0)
+    O.hier_refresh(H, rho, O.simp(rho, 3.0, 1e-9), k0, 3.0, 1e-9, 1.0)
+    return H
+
+
+@pytest.mark.parametrize("tag", ["t", "v", "w"])
+def test_multigrid_levels_transfers_cycle(tag):
+    g = golden("multigrid.npz")
+    H = _hier(g, tag)
+    assert len(H.levels) == int(g[f"{tag}_levels"])
+    assert H.vector_scalars == int(g[f"{tag}_vector_scalars"])
+    for l, lv in enumerate(H.levels):
+        assert np.array_equal(lv.scale, g[f"{tag}_scale{l}"])
+        assert np.array_equal(lv.diag, g[f"{tag}_diag{l}"])
+        assert np.array_equal(lv.fixed, g[f"{tag}_fixed{l}"])
+    for l in range(len(H.levels) - 1):
+        assert np.array_equal(O.restrict(H, l, g[f"{tag}_rf{l}"]), g[f"{tag}_rc{l}"])
+        assert np.array_equal(O.prolong(H, l, g[f"{tag}_ec{l}"]), g[f"{tag}_ef{l}"])
+    for l in range(1, len(H.levels)):
+        assert np.array_equal(O.level_apply(H, l, g[f"{tag}_cu{l}"]), g[f"{tag}_cv{l}"])
+    assert rel_err(O.coarse_solve(H, g[f"{tag}_fL"]), g[f"{tag}_uL"]) <= 1e-13
+    assert rel_err(O.jacobi(H, 0, g[f"{tag}_ju"], g[f"{tag}_f"], 2), g[f"{tag}_js"]) == 0.0
+    assert rel_err(O.vcycle(H, g[f"{tag}_f"]), g[f"{tag}_z"]) <= 1e-12
+
+
+@pytest.mark.parametrize("tag", ["u", "r"])
+def test_pcg_matches_reference(tag):
+    g = golden("pcg.npz")
+    case = O.cantilever_case(16, 8, 8)
+    es = case.es
+    rho = g[f"{tag}_rho"]
+    k0 = O.hex8_k0(0.3, case.h)
+    scale = O.simp(rho, 3.0, 1e-9)
+    fixed = np.flatnonzero(case.fixed_mask)
+    f = g["f"]
+    ref_f = case.f_ext.copy()
+    ref_f[fixed] = 0.0
+    assert np.array_equal(ref_f, f)
+    H = O.hier_build(es, case.h, case.fixed_mask, 3)
+    O.hier_refresh(H, rho, scale, k0, 3.0, 1e-9, 1.0)
+    ap = lambda v: O.apply_k(v, es, fixed, k0, scale)
+    rs = lambda v, ff: O.resid_k(v, ff, es, fixed, k0, scale)
+    for ctag, tol, maxit in (("a", 1e-5, 200), ("b", 1e-10, 500), ("c", 1e-12, 3), ("d", 1e-8, 120)):
+        u0 = g[f"{tag}{ctag}_u0"] if ctag == "d" else None
+        x, rep = O.pcg(ap, rs, lambda r: O.vcycle(H, r), f, u0, fixed, tol, maxit)
+        want = g[f"{tag}{ctag}_rep"]
+        assert rep.iterations == int(want[0])
+        assert rep.precond_applications == int(want[2])
+        assert bool(rep.converged) == bool(want[3])
+        assert abs(rep.final_rel_residual - want[1]) <= 1e-6 * want[1]
+        assert rel_err(x, g[f"{tag}{ctag}_x"]) <= 1e-9
+    d = np.diag(np.ones(1))  # silence linters
+    del d
+
+
+def test_design_kernels():
+    g = golden("design.npz")
+    es = (5, 6, 12)
+    h = 0.75
+    k0 = O.hex8_k0(0.3, h)
+    rho, u = g["rho"], g["u"]
+    dc = O.sensitivities(u, rho, es, k0, 3.0, 1e-9, 1.0)
+    assert rel_err(dc, g["dc"]) <= 1e-13
+    gu = O.gravity_unit(9.81, h, 0.7, 2)
+    dcg = O.sensitivities(u, rho, es, k0, 3.0, 1e-9, 1.0, gu)
+    assert rel_err(dcg, g["dcg"]) <= 1e-13
+    fixed = np.flatnonzero(face_fixed_mask(12, 6, 5))
+    assert np.array_equal(O.gravity_load(rho, es, gu, g["f_ext"], fixed), g["fgrav"])
+    assert np.array_equal(O.gravity_load(rho, es, gu), g["fgrav_plain"])
+    for tag, r in (("r15", 1.5 * h), ("r25", 2.5 * h), ("r18", 1.8 * h)):
+        kern = O.filter_kernel(h, r)
+        assert np.array_equal(kern, g[f"{tag}_kernel"])
+        wsum = O.correlate0(np.ones(rho.size), kern, es)
+        assert np.array_equal(wsum, g[f"{tag}_wsum"])
+        assert np.array_equal(O.filter_sens(g["dcin"], rho, kern, wsum, 1e-3, es), g[f"{tag}_dcf"])
+    act = g["oc_classes"] == 0
+    for tag, kw in (("a", dict(volfrac=0.3)), ("b", dict(volfrac=0.3, move=0.1, q=2.0)), ("c", dict(volfrac=0.25, eta=0.3))):
+        out, lam, steps = O.oc_update(g["oc_x0"], act, g["dcin"], np.ones(rho.size), **kw)
+        assert np.array_equal(out, g[f"oc{tag}_rho"])
+        assert lam == float(g[f"oc{tag}_lam"])
+        assert steps == int(g[f"oc{tag}_steps"])
+
+
+def _check_traj(recs, want, rho_ref=None, rho=None):
+    assert len(recs) == want.shape[0]
+    for rec, w in zip(recs, want):
+        assert rec.iteration == int(w[0])
+        assert rec.cg_iters == int(w[4])
+        assert abs(rec.compliance - w[1]) <= 1e-10 * abs(w[1])
+        assert rec.aux_scalars == int(w[6])
+    if rho_ref is not None:
+        assert np.abs(rho - rho_ref).max() <= 1e-8
+
+
+def test_small_trajectory():
+    g = golden("small_traj.npz")
+    case = O.cantilever_case(16, 8, 8)
+    rho, u, recs = O.run_design(case, 0.12, 2.5 * case.h, 30, max_levels=3, ch_tol=1e-12)
+    _check_traj(recs, g["recs"], g["rho30"], rho)
+
+
+def test_bridge_trajectory():
+    g = golden("bridge_traj.npz")
+    case = O.bridge_case(32, 16, 16)
+    rho, u, recs = O.run_design(case, 0.14, 1.5 * case.h, 3, ch_tol=1e-12)
+    _check_traj(recs, g["recs"], g["rho3"], rho)
+
+
+def test_gravity_trajectory_and_failure():
+    g = golden("grav_traj.npz")
+    case = O.cantilever_case(32, 16, 16, gravity=(2, 1.0, 1e-3))
+    rho, u, recs = O.run_design(case, 0.12, 1.5 * case.h, 4, ch_tol=1e-12)
+    _check_traj(recs, g["recs"], g["rho4"], rho)
+    info = json.load(open(os.path.join(GOLDEN, "grav_fail.json")))
+    case = O.cantilever_case(32, 16, 16, gravity=(2, 1.0, 1.0))
+    seen = []
+    with pytest.raises(O.OracleError) as ei:
+        O.run_design(case, 0.12, 1.5 * case.h, 4, ch_tol=1e-12, on_iter=lambda r, a, b: seen.append(r.compliance))
+    assert ei.value.kind == "volume" and info["raised"] == "VolumeInfeasible"
+    assert len(seen) == len(info["compliance"])
+    assert abs(seen[0] - info["compliance"][0]) <= 1e-10 * abs(seen[0])
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "cfg1_traj.npz")), reason="cfg1 fixture missing")
+@pytest.mark.slow
+def test_cfg1_trajectory_first_iterations():
+    g = golden("cfg1_traj.npz")
+    case = O.cantilever_case(48, 24, 24)
+    rho, u, recs = O.run_design(case, 0.12, 1.5 * case.h, 5, max_levels=4, ch_tol=1e-12)
+    _check_traj(recs, g["recs"][:5], g["rho5"], rho)
