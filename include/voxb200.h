@@ -1,0 +1,192 @@
+/*
+ * voxb200.h -- C ABI of the B200-native MGPCG hot path of voxtop
+ * (arXiv 2201.12931).  Implemented by paper_2201_12931_b200/libvoxb200.so
+ * (sm_100a CUDA kernels + a C++ runtime).  No torch types cross this
+ * boundary: device buffers are plain pointers, sizes are integers.
+ *
+ * The reference (/root/reference/pkg, package `voxtop` 0.1.0) is pure Python
+ * and has no FFI; each entry point below replaces one Python function of the
+ * reference hot path and cites it as  [ref: file:line]  (paths relative to
+ * pkg/src/voxtop/).  INTEGRATION.md shows the ctypes binding.
+ *
+ * ---------------------------------------------------------------- layouts
+ * Node vectors ("vt node layout") hold 3 doubles per node, components
+ * interleaved exactly like the reference dof numbering 3*node+comp
+ * [ref: grid.py:1-10], but rows are padded to an even node pitch (TMA needs
+ * 16-byte row strides) and the slab of node planes carries one ghost plane
+ * below and one above:
+ *     index(p, j, i, c) = ((p * (ny+1) + j) * row_pitch + i) * 3 + c,
+ *     p = k - k0 + 1 (k = global node plane, [k0, k1) = owned element layers).
+ * vt_vec_len() gives the length; vt_vec_upload/download convert to and from
+ * the reference's flat (n_dofs,) numpy order.  Pad entries and ghost planes
+ * must hold zeros (they do if the buffer was produced by this library or
+ * zero-initialised).
+ * Element fields passed by users (densities, sensitivities) are plain
+ * (n_elements,) arrays in the reference element order [ref: grid.py:75-82].
+ *
+ * ---------------------------------------------------------------- errors
+ * Every function returns a vt_status.  On failure vt_last_error() returns a
+ * message formatted like the reference's exception text; the Python layer
+ * maps the code to the reference exception class [ref: errors.py:7-24].
+ *
+ * All compute calls are asynchronous on `stream` (a cudaStream_t, NULL =
+ * legacy default) unless stated otherwise.  A handle is not thread safe.
+ */
+#ifndef VOXB200_H
+#define VOXB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VT_OK = 0,
+  VT_EINVAL = 1,        /* ValueError: shape / argument problems            */
+  VT_ECUDA = 2,         /* CUDA runtime or launch failure                     */
+  VT_ESETUP = 3,        /* SetupError  [ref: multigrid.py:280-316]            */
+  VT_EBREAKDOWN = 4,    /* SolverBreakdown [ref: solver.py:81-156, 183-187]   */
+  VT_EVOLUME = 5,       /* VolumeInfeasible [ref: optimize.py:271-292]        */
+  VT_ENUMERICAL = 6,    /* NumericalError                                     */
+  VT_ENOMEM = 7,        /* device allocation failure                          */
+  VT_EDENSITY = 8       /* ValueError "density outside [0, 1]" [ref: element.py:105-106] */
+} vt_status;
+
+const char *vt_last_error(void);
+int vt_version(void);
+/* Number of CUDA kernel launches issued by this library since load (the
+ * bench reports it as gpu_launches). */
+uint64_t vt_launch_count(void);
+/* device-to-device byte copy on stream (helper for bindings without a CUDA runtime) */
+vt_status vt_copy(void *dst, const void *src, int64_t bytes, void *stream);
+
+/* ------------------------------------------------------------------ grid
+ * A vt_grid is one structured hex8 grid on one device: geometry, material
+ * constants (nu, h), the fixed-dof mask, and scratch (reduction partials,
+ * TMA descriptor cache).  Replaces the static part of OperatorState
+ * [ref: operator.py:108-151] and StructuredGrid [ref: grid.py:45-111].
+ *
+ * node_mask: host array of (nz+1)*(ny+1)*(nx+1) bytes, bit c set <=> dof
+ * 3*node+c is fixed.  k0/k1: owned element layers of this rank's z-slab
+ * (0, nz for a single GPU).
+ */
+typedef struct vt_grid vt_grid;
+
+vt_status vt_grid_create(vt_grid **out, int nx, int ny, int nz, double h, double nu,
+                         const uint8_t *node_mask, int k0, int k1, int device);
+vt_status vt_grid_destroy(vt_grid *g);
+int64_t vt_vec_len(const vt_grid *g);   /* doubles in a vt node-layout vector  */
+int64_t vt_elem_len(const vt_grid *g);  /* doubles in a vt element-layout field */
+int64_t vt_n_fixed(const vt_grid *g);   /* fixed dofs of this slab              */
+
+/* host <-> device conversion between the reference order and vt layout.
+ * host pointers may be pageable or pinned; these calls are async on stream. */
+vt_status vt_vec_upload(const vt_grid *g, const double *host, double *dev, void *stream);
+vt_status vt_vec_download(const vt_grid *g, const double *dev, double *host, void *stream);
+
+/* scale = E * (kmin + rho^p (1 - kmin)) into vt element layout (ghost layer
+ * and padding zero) [ref: operator.py:142, element.py:102-108].  rho is a
+ * plain device array of n_elements doubles.  Fails with VT_EDENSITY when a
+ * density lies outside [0, 1] (synchronises to report it). */
+vt_status vt_scale_from_density(vt_grid *g, const double *rho, double p, double kmin,
+                                double E, double *scale, void *stream);
+
+/* ---------------------------------------------------------- operator
+ * v = K(rho) u with identity on fixed dofs; u is projected to zero on fixed
+ * dofs before the product [ref: operator.py:58-81, 154-165]. */
+vt_status vt_apply(vt_grid *g, const double *scale, const double *u, double *v, void *stream);
+/* d = diag K, 1 on fixed [ref: operator.py:84-105, 168-174] */
+vt_status vt_diagonal(vt_grid *g, const double *scale, double *d, void *stream);
+/* r = f - K u, zero on fixed [ref: operator.py:177-184] */
+vt_status vt_residual(vt_grid *g, const double *scale, const double *u, const double *f,
+                      double *r, void *stream);
+/* out = x . y over this slab's owned dofs (deterministic order); blocking. */
+vt_status vt_dot(vt_grid *g, const double *x, const double *y, double *out, void *stream);
+
+/* ---------------------------------------------------------- multigrid
+ * Homogenized geometric multigrid [ref: multigrid.py:150-499].  Level 0 is
+ * `fine`; levels are created by halving, coarse fixed dofs = fine fixed dofs
+ * at even nodes [ref: multigrid.py:137-141]. */
+typedef struct vt_hier vt_hier;
+
+vt_status vt_hier_create(vt_hier **out, vt_grid *fine, int n_levels, double omega, int sweeps);
+vt_status vt_hier_destroy(vt_hier *H);
+int vt_hier_levels(const vt_hier *H);
+vt_grid *vt_hier_grid(vt_hier *H, int level);
+/* coarse element densities + scales + per-level diagonal + coarsest direct
+ * factor [ref: multigrid.py:201-233, 280-316]; rho: plain fine densities,
+ * scale0: fine scale in vt element layout. */
+vt_status vt_hier_refresh(vt_hier *H, const double *rho, const double *scale0, double p,
+                          double kmin, double E, void *stream);
+/* z = V-cycle(f) [ref: multigrid.py:404-430] */
+vt_status vt_hier_vcycle(vt_hier *H, const double *f, double *z, void *stream);
+/* level-l building blocks (tests / API parity) */
+vt_status vt_hier_restrict(vt_hier *H, int l, const double *fine, double *coarse, void *stream);
+vt_status vt_hier_prolong(vt_hier *H, int l, const double *coarse, double *fine, void *stream);
+vt_status vt_hier_jacobi(vt_hier *H, int l, const double *u, const double *f, int sweeps,
+                         double *out, void *stream);
+vt_status vt_hier_level_apply(vt_hier *H, int l, const double *u, double *v, void *stream);
+vt_status vt_hier_level_diag(vt_hier *H, int l, double *d, void *stream);
+vt_status vt_hier_coarse_solve(vt_hier *H, const double *f, double *u, void *stream);
+/* device pointer to level-l element scale / plain density (vt layouts) */
+const double *vt_hier_level_scale(vt_hier *H, int l);
+const double *vt_hier_level_rho(vt_hier *H, int l);
+
+/* ---------------------------------------------------------- solver
+ * Preconditioned CG with the reference recurrences, true residual every 50
+ * iterations and on convergence, and identical breakdown checks
+ * [ref: solver.py:62-167]; precond: 0 none, 1 Jacobi [ref: solver.py:57-59],
+ * 2 multigrid V-cycle (H required) [ref: solver.py:170-191].
+ * x: in = warm start (ignored unless warm), out = solution.  Blocking. */
+typedef struct {
+  int iterations;
+  double final_rel_residual;
+  int precond_applications;
+  int converged;
+  double residual_drift;
+  int breakdown;          /* 0 none; 1 rz<=0 (it 0 or k); 2 non-finite pq; 3 pq<=0; 4 non-finite residual; 5 non-finite rhs */
+  int breakdown_iter;
+  double breakdown_value;
+} vt_solve_report;
+
+vt_status vt_pcg(vt_grid *g, const double *scale, int precond, vt_hier *H, const double *f,
+                 double *x, int warm, double tol, int max_iterations, vt_solve_report *rep,
+                 void *stream);
+
+/* ---------------------------------------------------------- design loop
+ * [ref: optimize.py:186-302] */
+/* c = f . u (blocking) */
+vt_status vt_compliance(vt_grid *g, const double *f, const double *u, double *c, void *stream);
+/* dc_e = -E s'(rho_e) u_e'K0 u_e (+ 2 u_e.g_unit when grav_axis >= 0), plain
+ * element order [ref: optimize.py:195-213]; grav_coef = -uw*g*h^3/8 */
+vt_status vt_sensitivities(vt_grid *g, const double *u, const double *rho, double p, double kmin,
+                           double E, int grav_axis, double grav_coef, double *dc, void *stream);
+/* f = scatter(rho_e g_unit) (+ f_ext) (zero on fixed if zero_fixed)
+ * [ref: optimize.py:216-231] */
+vt_status vt_gravity_load(vt_grid *g, const double *rho, int grav_axis, double grav_coef,
+                          const double *f_ext, int zero_fixed, double *f, void *stream);
+/* sensitivity filter with a (2R+1)^3 kernel in (dk,dj,di) order; wsum is
+ * computed on the device at creation [ref: optimize.py:110-179] */
+typedef struct vt_filter vt_filter;
+vt_status vt_filter_create(vt_filter **out, vt_grid *g, int R, const double *kernel_host);
+vt_status vt_filter_destroy(vt_filter *F);
+const double *vt_filter_wsum(vt_filter *F);
+vt_status vt_filter_apply(vt_filter *F, const double *dc, const double *rho, double gamma,
+                          double *dcf, void *stream);
+/* out = correlate(field, kernel), zero padding [ref: optimize.py:139-144] */
+vt_status vt_filter_correlate(vt_filter *F, const double *field, double *out, void *stream);
+/* OC update with bisected multiplier [ref: optimize.py:245-302]; classes:
+ * int8 per element (0 active).  Blocking; VT_EVOLUME on infeasibility. */
+vt_status vt_oc_update(vt_grid *g, const double *rho, const int8_t *classes, const double *dc,
+                       const double *dv, double volfrac, double move, double eta, double q,
+                       double *rho_out, double *lam, int *steps, void *stream);
+/* max |a-b| and mean of a over active elements (blocking helpers of run()) */
+vt_status vt_change_volume(vt_grid *g, const double *a, const double *b, const int8_t *classes,
+                           double *max_abs_diff, double *active_mean, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXB200_H */

@@ -1,0 +1,647 @@
+// Homogenized geometric multigrid on B200 [ref: multigrid.py:84-499].
+//
+//  * restriction / prolongation reproduce the reference's separable axis
+//    passes (z, then y, then x) operation for operation, so the transfers
+//    are bit-identical to numpy [ref: multigrid.py:341-371, 433-459];
+//  * coarse densities are the pairwise mean of the 8 children exactly as
+//    numpy's mean(axis=1) rounds it [ref: multigrid.py:94-104, 209-215];
+//  * the coarsest level is factored on the device (dense Cholesky) and
+//    inverted once per refresh, so each V-cycle's coarse solve is one
+//    deterministic dense mat-vec [ref: multigrid.py:280-316, 395-402].
+#include <math.h>
+
+#include <vector>
+
+#include "vt_internal.h"
+#include "vt_pcg.cuh"
+
+namespace vt {
+
+constexpr int MG_THREADS = 256;
+
+__device__ __forceinline__ bool node_coords(const Geom& g, long long t, int& p, int& j, int& i) {
+  i = (int)(t % (g.nx + 1));
+  const long long r = t / (g.nx + 1);
+  j = (int)(r % (g.ny + 1));
+  p = (int)(r / (g.ny + 1)) + g.pA;
+  return true;
+}
+__device__ __forceinline__ long long owned_nodes(const Geom& g) {
+  return (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
+}
+
+// ---------------------------------------------------------------- SIMP scale
+__device__ __forceinline__ double simp_pow(double r, double p) {
+  if (p == 3.0) {  // correctly rounded r^3 (numpy's pow agrees in ~95% of cases, else 1 ulp)
+    const double hi = r * r;
+    const double lo = fma(r, r, -hi);
+    return fma(hi, r, lo * r);
+  }
+  if (p == 2.0) return r * r;
+  if (p == 1.0) return r;
+  if (p == 0.5) return sqrt(r);
+  if (p == 0.0) return 1.0;
+  return pow(r, p);
+}
+
+__global__ void scale_kernel(Geom g, const double* rho, double p, double kmin, double E,
+                             double* scale, int* bad) {
+  const long long nel = (long long)g.nx * g.ny * (g.k1 - g.k0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % g.nx);
+    const long long r = e / g.nx;
+    const int j = (int)(r % g.ny);
+    const int q = (int)(r / g.ny) + 1;
+    const double x = rho[e];
+    if (!(x >= 0.0 && x <= 1.0)) *bad = 1;
+    // E * (kmin + r**p * (1 - kmin))  [ref: element.py:107, operator.py:142]
+    const double s = __dmul_rn(E, __dadd_rn(kmin, __dmul_rn(simp_pow(x, p), 1.0 - kmin)));
+    scale[elem_off(g, q, j, i)] = s;
+  }
+}
+
+vt_status launch_scale(vt_grid* G, const double* rho, double p, double kmin, double E,
+                       double* scale, int* bad, cudaStream_t s) {
+  scale_kernel<<<G->nsm * 8, MG_THREADS, 0, s>>>(G->g, rho, p, kmin, E, scale, bad);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// ---------------------------------------------------------------- coarsening
+// rho_c = mean of the 8 children, numpy pairwise order
+__global__ void coarsen_rho_kernel(int fnx, int fny, int cnx, int cny, int cnz,
+                                   const double* __restrict__ rf, double* __restrict__ rc) {
+  const long long nel = (long long)cnx * cny * cnz;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % cnx);
+    const long long r = e / cnx;
+    const int j = (int)(r % cny);
+    const int k = (int)(r / cny);
+    double ch[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const long long fi = 2 * i + (c & 1), fj = 2 * j + ((c >> 1) & 1), fk = 2 * k + (c >> 2);
+      ch[c] = rf[(fk * fny + fj) * fnx + fi];
+    }
+    const double s = __dadd_rn(__dadd_rn(__dadd_rn(ch[0], ch[1]), __dadd_rn(ch[2], ch[3])),
+                               __dadd_rn(__dadd_rn(ch[4], ch[5]), __dadd_rn(ch[6], ch[7])));
+    rc[e] = s / 8.0;
+  }
+}
+
+// coarse dof fixed <=> coincident fine dof fixed [ref: multigrid.py:137-141]
+__global__ void coarsen_mask_kernel(Geom gf, Geom gc, const uint8_t* mf, uint8_t* mc) {
+  const long long nn = owned_nodes(gc);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    int p, j, i;
+    node_coords(gc, t, p, j, i);
+    const int K = p - 1 + gc.k0;
+    const int pf = 2 * K - gf.k0 + 1;
+    mc[node_off(gc, p, j, i)] = mf[node_off(gf, pf, 2 * j, 2 * i)];
+  }
+}
+
+__global__ void count_fixed_kernel(Geom g, const uint8_t* m, unsigned long long* out) {
+  const long long nn = owned_nodes(g);
+  unsigned long long c = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    int p, j, i;
+    node_coords(g, t, p, j, i);
+    c += __popc((unsigned)m[node_off(g, p, j, i)] & 7u);
+  }
+  atomicAdd(out, c);  // integer: order-independent
+}
+
+// ---------------------------------------------------------------- transfers
+// f_c = P^T r_f, coarse fixed zeroed.  Per axis (z, y, x):
+//   dst[i] = (src[2i] + 0.5 src[2i+1]) + 0.5 src[2i-1]   (missing terms skipped)
+__global__ void restrict_kernel(Geom gf, Geom gc, const uint8_t* mc, const double* __restrict__ rf,
+                                double* __restrict__ fc, const int* stop) {
+  if (stop && *(volatile const int*)stop) return;
+  const long long nn = owned_nodes(gc);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    int p, J, I;
+    node_coords(gc, t, p, J, I);
+    const int K = p - 1 + gc.k0;
+    const long long cnode = node_off(gc, p, J, I);
+    const unsigned m = mc[cnode];
+    double out[3];
+    // y/x neighbourhood of fine node (2J, 2I); index 0 = centre, 1 = +1, 2 = -1
+    const int fj[3] = {2 * J, 2 * J + 1, 2 * J - 1};
+    const int fi[3] = {2 * I, 2 * I + 1, 2 * I - 1};
+    const int fk[3] = {2 * K, 2 * K + 1, 2 * K - 1};
+    bool okj[3], oki[3], okk[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      okj[a] = fj[a] >= 0 && fj[a] <= gf.ny;
+      oki[a] = fi[a] >= 0 && fi[a] <= gf.nx;
+      okk[a] = fk[a] >= 0 && fk[a] <= gf.nz;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double ty[3];  // after z and y passes, per x position
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        ty[b] = 0.0;
+        if (!oki[b]) continue;
+        double tz[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          tz[a] = 0.0;
+          if (!okj[a]) continue;
+          auto R = [&](int kk) {
+            const int pf = kk - gf.k0 + 1;
+            return rf[node_off(gf, pf, fj[a], fi[b]) * 3 + c];
+          };
+          double v = R(fk[0]);
+          if (okk[1]) v = __dadd_rn(v, 0.5 * R(fk[1]));
+          if (okk[2]) v = __dadd_rn(v, 0.5 * R(fk[2]));
+          tz[a] = v;
+        }
+        double v = tz[0];
+        if (okj[1]) v = __dadd_rn(v, 0.5 * tz[1]);
+        if (okj[2]) v = __dadd_rn(v, 0.5 * tz[2]);
+        ty[b] = v;
+      }
+      double v = ty[0];
+      if (oki[1]) v = __dadd_rn(v, 0.5 * ty[1]);
+      if (oki[2]) v = __dadd_rn(v, 0.5 * ty[2]);
+      out[c] = ((m >> c) & 1u) ? 0.0 : v;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fc[cnode * 3 + c] = out[c];
+  }
+}
+
+// u_f (+)= P u_c with fine fixed dofs zeroed in P u_c.  Per axis (z, y, x):
+//   even: dst = src[i/2];  odd: dst = 0.5 * (src[(i-1)/2] + src[(i+1)/2])
+template <bool ADD>
+__global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double* __restrict__ uc,
+                               double* __restrict__ uf, const int* stop) {
+  if (stop && *(volatile const int*)stop) return;
+  const long long nn = owned_nodes(gf);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    int p, j, i;
+    node_coords(gf, t, p, j, i);
+    const int k = p - 1 + gf.k0;
+    const long long fnode = node_off(gf, p, j, i);
+    const unsigned m = mf[fnode];
+    const int kz0 = k >> 1, kz1 = (k + 1) >> 1;
+    const int jy0 = j >> 1, jy1 = (j + 1) >> 1;
+    const int ix0 = i >> 1, ix1 = (i + 1) >> 1;
+    const bool oz = k & 1, oy = j & 1, ox = i & 1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      auto Z = [&](int ix, int iy) {
+        const double a = uc[node_off(gc, kz0 - gc.k0 + 1, iy, ix) * 3 + c];
+        if (!oz) return a;
+        const double b = uc[node_off(gc, kz1 - gc.k0 + 1, iy, ix) * 3 + c];
+        return 0.5 * __dadd_rn(a, b);
+      };
+      auto Y = [&](int ix) {
+        const double a = Z(ix, jy0);
+        if (!oy) return a;
+        return 0.5 * __dadd_rn(a, Z(ix, jy1));
+      };
+      double v = Y(ix0);
+      if (ox) v = 0.5 * __dadd_rn(v, Y(ix1));
+      if ((m >> c) & 1u) v = 0.0;
+      if (ADD)
+        uf[fnode * 3 + c] = __dadd_rn(uf[fnode * 3 + c], v);
+      else
+        uf[fnode * 3 + c] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- coarsest level
+// Dense assembly (identity on fixed), in-place Cholesky; one CTA.
+// [ref: multigrid.py:280-316]
+__global__ void __launch_bounds__(1024, 1)
+    coarse_factor_kernel(Geom g, const double* scale, const double* k0l, const uint8_t* mask,
+                         int n, double* A, int* status) {
+  const int nx1 = g.nx + 1, ny1 = g.ny + 1;
+  for (long long t = threadIdx.x; t < (long long)n * n; t += blockDim.x) A[t] = 0.0;
+  __syncthreads();
+  const int nel = g.nx * g.ny * g.nz;
+  for (int e = 0; e < nel; ++e) {
+    const int i = e % g.nx, j = (e / g.nx) % g.ny, k = e / (g.nx * g.ny);
+    const double s = scale[elem_off(g, k + 1, j, i)];
+    for (int t = threadIdx.x; t < 576; t += blockDim.x) {
+      const int a = t / 24, b = t % 24;
+      const int ca = a / 3, cb = b / 3;
+      const int na = (i + (ca & 1)) + (j + ((ca >> 1) & 1)) * nx1 + (k + (ca >> 2)) * nx1 * ny1;
+      const int nb = (i + (cb & 1)) + (j + ((cb >> 1) & 1)) * nx1 + (k + (cb >> 2)) * nx1 * ny1;
+      const int da = 3 * na + a % 3, db = 3 * nb + b % 3;
+      A[(long long)da * n + db] += s * k0l[t];
+    }
+    __syncthreads();
+  }
+  // identity rows / columns on fixed dofs
+  for (int d = threadIdx.x; d < n; d += blockDim.x) {
+    const int node = d / 3, c = d % 3;
+    const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
+    if ((mask[node_off(g, k + 1, j, i)] >> c) & 1u) {
+      for (int e = 0; e < n; ++e) A[(long long)d * n + e] = 0.0;
+    }
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < n; d += blockDim.x) {
+    for (int e = 0; e < n; ++e) {
+      const int node = e / 3, c = e % 3;
+      const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
+      if ((mask[node_off(g, k + 1, j, i)] >> c) & 1u) A[(long long)d * n + e] = (d == e) ? 1.0 : 0.0;
+    }
+  }
+  __syncthreads();
+  // right-looking Cholesky, lower triangle
+  __shared__ double piv;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = A[(long long)j * n + j];
+      if (!(d > 0.0) || !isfinite(d)) {
+        bad = 1;
+        piv = 1.0;
+      } else {
+        piv = sqrt(d);
+      }
+      A[(long long)j * n + j] = piv;
+    }
+    __syncthreads();
+    if (bad) break;
+    const double lj = piv;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) A[(long long)i * n + j] /= lj;
+    __syncthreads();
+    const long long m = n - j - 1;
+    for (long long t = threadIdx.x; t < m * m; t += blockDim.x) {
+      const int ii = j + 1 + (int)(t / m), kk = j + 1 + (int)(t % m);
+      if (kk <= ii) A[(long long)ii * n + kk] -= A[(long long)ii * n + j] * A[(long long)kk * n + j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *status = bad;
+}
+
+// W = L^{-1}: one thread per column
+__global__ void tri_inverse_kernel(int n, const double* A, double* W) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  for (int i = 0; i < c; ++i) W[(long long)i * n + c] = 0.0;
+  for (int i = c; i < n; ++i) {
+    double s = (i == c) ? 1.0 : 0.0;
+    for (int k = c; k < i; ++k) s -= A[(long long)i * n + k] * W[(long long)k * n + c];
+    W[(long long)i * n + c] = s / A[(long long)i * n + i];
+  }
+}
+
+// Kinv = W^T W
+__global__ void gram_kernel(int n, const double* W, double* Kinv) {
+  const long long nn = (long long)n * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / n), j = (int)(t % n);
+    double s = 0.0;
+    for (int k = max(i, j); k < n; ++k) s = fma(W[(long long)k * n + i], W[(long long)k * n + j], s);
+    Kinv[t] = s;
+  }
+}
+
+// u = Kinv f on the coarsest level (vt layout in / out, fixed dofs 0)
+__global__ void coarse_solve_kernel(Geom g, const uint8_t* mask, int n, const double* Kinv,
+                                    const double* f, double* u, const int* stop) {
+  if (stop && *(volatile const int*)stop) return;
+  extern __shared__ double fc[];
+  const int nx1 = g.nx + 1, ny1 = g.ny + 1;
+  for (int d = threadIdx.x; d < n; d += blockDim.x) {
+    const int node = d / 3, c = d % 3;
+    const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
+    fc[d] = f[node_off(g, k + 1, j, i) * 3 + c];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int r = blockIdx.x * nw + warp; r < n; r += gridDim.x * nw) {
+    double s = 0.0;
+    for (int e = lane; e < n; e += 32) s = fma(Kinv[(long long)r * n + e], fc[e], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int node = r / 3, c = r % 3;
+      const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
+      const long long nd = node_off(g, k + 1, j, i);
+      u[nd * 3 + c] = ((mask[nd] >> c) & 1u) ? 0.0 : s;
+    }
+  }
+}
+
+}  // namespace vt
+
+// ====================================================================== hierarchy
+struct vt_hier {
+  std::vector<vt_grid*> lv;        // lv[0] = caller's fine grid (not owned)
+  std::vector<double*> u, u2, r, f, scale, rho;
+  double omega = 0.4;
+  int sweeps = 1;
+  int nL = 0;                      // coarsest dofs
+  double *A = nullptr, *W = nullptr, *Kinv = nullptr, *k0l = nullptr;
+  int* status = nullptr;
+  bool factored = false;
+  const double* last_z = nullptr;  // buffer that holds the V-cycle output
+};
+
+namespace vt {
+
+vt_status hier_alloc_vec(vt_grid* G, double** p) {
+  VT_CUDA(cudaMalloc(p, G->vec_len() * sizeof(double)));
+  VT_CUDA(cudaMemset(*p, 0, G->vec_len() * sizeof(double)));
+  return VT_OK;
+}
+
+void hex8_k0_host(double nu, double h, double* K);  // runtime.cu
+
+// Build the level sequence of one V-cycle on `s` (capturable).
+vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, double* rz_partial,
+                             bool want_rz, cudaStream_t s, const double** z_out) {
+  const int L = (int)H->lv.size();
+  std::vector<const double*> fl(L);
+  std::vector<double*> ucur(L);
+  fl[0] = f0;
+  for (int l = 1; l < L; ++l) fl[l] = H->f[l];
+  auto smooth = [&](int l, bool dot) -> vt_status {
+    vt_grid* G = H->lv[l];
+    double* dst = (ucur[l] == H->u[l]) ? H->u2[l] : H->u[l];
+    VT_TRY(launch_hex8(G, H8_SMOOTH, dot, H->scale[l], ucur[l], ucur[l], fl[l], dst, H->omega,
+                       rz_partial, stop, s));
+    ucur[l] = dst;
+    return VT_OK;
+  };
+  for (int l = 0; l < L - 1; ++l) {
+    vt_grid* G = H->lv[l];
+    ucur[l] = H->u[l];
+    if (H->sweeps >= 1) {
+      VT_TRY(launch_jacobi0(G, H->scale[l], H->omega, fl[l], H->u[l], stop, s));
+      for (int k = 1; k < H->sweeps; ++k) VT_TRY(smooth(l, false));
+      VT_TRY(launch_hex8(G, H8_RESID, false, H->scale[l], ucur[l], ucur[l], fl[l], H->r[l], 0.0,
+                         nullptr, stop, s));
+      restrict_kernel<<<H->lv[l + 1]->nsm * 4, MG_THREADS, 0, s>>>(
+          G->g, H->lv[l + 1]->g, H->lv[l + 1]->mask, H->r[l], H->f[l + 1], stop);
+    } else {
+      VT_TRY(launch_zero_owned(G, H->u[l], s));
+      restrict_kernel<<<H->lv[l + 1]->nsm * 4, MG_THREADS, 0, s>>>(
+          G->g, H->lv[l + 1]->g, H->lv[l + 1]->mask, fl[l], H->f[l + 1], stop);
+    }
+    count_launch();
+    VT_CUDA(cudaGetLastError());
+  }
+  {
+    vt_grid* G = H->lv[L - 1];
+    const size_t sm = (size_t)H->nL * sizeof(double);
+    coarse_solve_kernel<<<(H->nL + 255) / 256 > 32 ? 32 : (H->nL + 255) / 256, 256, sm, s>>>(
+        G->g, G->mask, H->nL, H->Kinv, fl[L - 1], H->u[L - 1], stop);
+    count_launch();
+    VT_CUDA(cudaGetLastError());
+    ucur[L - 1] = H->u[L - 1];
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    vt_grid* G = H->lv[l];
+    prolong_kernel<true><<<G->nsm * 8, MG_THREADS, 0, s>>>(H->lv[l + 1]->g, G->g, G->mask,
+                                                           ucur[l + 1], ucur[l], stop);
+    count_launch();
+    VT_CUDA(cudaGetLastError());
+    for (int k = 0; k < H->sweeps; ++k) VT_TRY(smooth(l, want_rz && l == 0 && k == H->sweeps - 1));
+  }
+  *z_out = ucur[0];
+  H->last_z = ucur[0];
+  return VT_OK;
+}
+
+// number of partials the V-cycle's rz dot leaves (0 if it cannot fuse it)
+int hier_rz_parts(vt_hier* H) {
+  if (H->lv.size() < 2 || H->sweeps < 1) return 0;
+  return H->lv[0]->h8.grid;
+}
+
+}  // namespace vt
+
+using namespace vt;
+
+extern "C" {
+
+vt_status vt_hier_create(vt_hier** out, vt_grid* fine, int n_levels, double omega, int sweeps) {
+  if (!out || !fine) return fail(VT_EINVAL, "null argument");
+  if (n_levels < 1) return fail(VT_EINVAL, "max_levels must be at least 1");
+  if (!(omega > 0.0 && omega <= 1.0))
+    return fail(VT_EINVAL, "jacobi damping must lie in (0, 1]");
+  if (sweeps < 0) return fail(VT_EINVAL, "sweeps must be non-negative");
+  if (fine->g.k0 != 0 || fine->g.k1 != fine->g.nz)
+    return fail(VT_EINVAL, "multi-slab hierarchies are built by the distributed runtime");
+  VT_CUDA(cudaSetDevice(fine->device));
+  vt_hier* H = new vt_hier();
+  H->omega = omega;
+  H->sweeps = sweeps;
+  H->lv.push_back(fine);
+  int nx = fine->g.nx, ny = fine->g.ny, nz = fine->g.nz;
+  double h = fine->h;
+  for (int l = 1; l < n_levels; ++l) {
+    nx /= 2; ny /= 2; nz /= 2; h *= 2.0;
+    vt_grid* c = nullptr;
+    vt_status st = vt_grid_create(&c, nx, ny, nz, h, fine->nu, nullptr, 0, nz, fine->device);
+    if (st != VT_OK) { vt_hier_destroy(H); return st; }
+    vt_grid* f = H->lv.back();
+    coarsen_mask_kernel<<<c->nsm * 4, MG_THREADS>>>(f->g, c->g, f->mask, c->mask);
+    count_launch();
+    unsigned long long* cnt;
+    VT_CUDA(cudaMalloc(&cnt, sizeof(unsigned long long)));
+    VT_CUDA(cudaMemset(cnt, 0, sizeof(unsigned long long)));
+    count_fixed_kernel<<<c->nsm, MG_THREADS>>>(c->g, c->mask, cnt);
+    count_launch();
+    unsigned long long hc = 0;
+    VT_CUDA(cudaMemcpy(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost));
+    VT_CUDA(cudaFree(cnt));
+    c->n_fixed = (long long)hc;
+    H->lv.push_back(c);
+  }
+  const int L = (int)H->lv.size();
+  H->u.assign(L, nullptr); H->u2.assign(L, nullptr); H->r.assign(L, nullptr);
+  H->f.assign(L, nullptr); H->scale.assign(L, nullptr); H->rho.assign(L, nullptr);
+  for (int l = 0; l < L; ++l) {
+    vt_grid* G = H->lv[l];
+    VT_TRY(hier_alloc_vec(G, &H->u[l]));
+    VT_TRY(hier_alloc_vec(G, &H->u2[l]));
+    VT_TRY(hier_alloc_vec(G, &H->r[l]));
+    if (l > 0) VT_TRY(hier_alloc_vec(G, &H->f[l]));
+    VT_CUDA(cudaMalloc(&H->scale[l], G->elem_len() * sizeof(double)));
+    VT_CUDA(cudaMemset(H->scale[l], 0, G->elem_len() * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->rho[l], (size_t)G->nel_local() * sizeof(double)));
+  }
+  vt_grid* C = H->lv.back();
+  H->nL = (int)(3LL * (C->g.nx + 1) * (C->g.ny + 1) * (C->g.nz + 1));
+  *out = H;
+  return VT_OK;
+}
+
+vt_status vt_hier_destroy(vt_hier* H) {
+  if (!H) return VT_OK;
+  for (size_t l = 0; l < H->lv.size(); ++l) {
+    cudaFree(H->u[l]); cudaFree(H->u2[l]); cudaFree(H->r[l]);
+    if (l > 0) cudaFree(H->f[l]);
+    cudaFree(H->scale[l]); cudaFree(H->rho[l]);
+    if (l > 0) vt_grid_destroy(H->lv[l]);
+  }
+  cudaFree(H->A); cudaFree(H->W); cudaFree(H->Kinv); cudaFree(H->k0l); cudaFree(H->status);
+  delete H;
+  return VT_OK;
+}
+
+int vt_hier_levels(const vt_hier* H) { return H ? (int)H->lv.size() : 0; }
+vt_grid* vt_hier_grid(vt_hier* H, int l) {
+  return (H && l >= 0 && l < (int)H->lv.size()) ? H->lv[l] : nullptr;
+}
+const double* vt_hier_level_scale(vt_hier* H, int l) { return H->scale[l]; }
+const double* vt_hier_level_rho(vt_hier* H, int l) { return H->rho[l]; }
+
+vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, double p,
+                          double kmin, double E, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int L = (int)H->lv.size();
+  vt_grid* F = H->lv[0];
+  VT_CUDA(cudaMemcpyAsync(H->scale[0], scale0, F->elem_len() * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s));
+  VT_CUDA(cudaMemcpyAsync(H->rho[0], rho, F->nel_local() * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s));
+  int* bad = reinterpret_cast<int*>(F->scalars);
+  VT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  for (int l = 1; l < L; ++l) {
+    vt_grid* f = H->lv[l - 1];
+    vt_grid* c = H->lv[l];
+    coarsen_rho_kernel<<<c->nsm * 4, MG_THREADS, 0, s>>>(f->g.nx, f->g.ny, c->g.nx, c->g.ny,
+                                                         c->g.nz, H->rho[l - 1], H->rho[l]);
+    count_launch();
+    VT_TRY(launch_scale(c, H->rho[l], p, kmin, E, H->scale[l], bad, s));
+  }
+  // coarsest direct factor
+  vt_grid* C = H->lv.back();
+  const int n = H->nL;
+  if (n > 20000)
+    return fail(VT_ESETUP, "coarsest level has " + std::to_string(n) +
+                               " dofs, above the direct-solve guard 20000; increase the level count");
+  if (L > 1 && C->n_fixed < 6)
+    return fail(VT_ESETUP, "only " + std::to_string(C->n_fixed) +
+                               " fixed dofs survive on the coarsest level; rigid modes are "
+                               "unconstrained (bad fixed-dof coarsening)");
+  if (!H->A) {
+    VT_CUDA(cudaMalloc(&H->A, (size_t)n * n * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->W, (size_t)n * n * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->Kinv, (size_t)n * n * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->k0l, 576 * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->status, sizeof(int)));
+    double K[576];
+    hex8_k0_host(C->nu, C->h, K);
+    VT_CUDA(cudaMemcpy(H->k0l, K, sizeof(K), cudaMemcpyHostToDevice));
+    if ((size_t)n * sizeof(double) > 48 * 1024)
+      VT_CUDA(cudaFuncSetAttribute(coarse_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(n * sizeof(double))));
+  }
+  coarse_factor_kernel<<<1, 1024, 0, s>>>(C->g, H->scale[L - 1], H->k0l, C->mask, n, H->A,
+                                          H->status);
+  tri_inverse_kernel<<<(n + 127) / 128, 128, 0, s>>>(n, H->A, H->W);
+  gram_kernel<<<C->nsm * 4, 256, 0, s>>>(n, H->W, H->Kinv);
+  count_launch(3);
+  VT_CUDA(cudaGetLastError());
+  int hb[2] = {0, 0};
+  VT_CUDA(cudaMemcpyAsync(&hb[0], bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  VT_CUDA(cudaMemcpyAsync(&hb[1], H->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  VT_CUDA(cudaStreamSynchronize(s));
+  if (hb[0]) return fail(VT_EDENSITY, "density outside [0, 1]");
+  if (hb[1])
+    return fail(VT_ESETUP,
+                "coarsest-level matrix is not positive definite; the fixed dof set may vanish "
+                "under coarsening");
+  H->factored = true;
+  return VT_OK;
+}
+
+vt_status vt_hier_vcycle(vt_hier* H, const double* f, double* z, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!H->factored) return fail(VT_ESETUP, "hierarchy was not refreshed before use");
+  vt_grid* F = H->lv[0];
+  // fine.f = f with fixed dofs zeroed [ref: multigrid.py:413-414]
+  VT_TRY(launch_project(F, f, F->scratch, s));
+  const double* zb = nullptr;
+  VT_TRY(hier_vcycle_launch(H, F->scratch, nullptr, nullptr, false, s, &zb));
+  VT_CUDA(cudaMemcpyAsync(z, zb, F->vec_len() * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return VT_OK;
+}
+
+vt_status vt_hier_restrict(vt_hier* H, int l, const double* fine, double* coarse, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (l < 0 || l + 1 >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
+  vt_grid* F = H->lv[l];
+  VT_TRY(launch_project(F, fine, F->scratch, s));
+  restrict_kernel<<<H->lv[l + 1]->nsm * 4, MG_THREADS, 0, s>>>(F->g, H->lv[l + 1]->g,
+                                                               H->lv[l + 1]->mask, F->scratch,
+                                                               coarse, nullptr);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status vt_hier_prolong(vt_hier* H, int l, const double* coarse, double* fine, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (l < 0 || l + 1 >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
+  vt_grid* F = H->lv[l];
+  prolong_kernel<false><<<F->nsm * 8, MG_THREADS, 0, s>>>(H->lv[l + 1]->g, F->g, F->mask, coarse,
+                                                          fine, nullptr);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status vt_hier_jacobi(vt_hier* H, int l, const double* u, const double* f, int sweeps,
+                         double* out, void* stream) {
+  // out-of-place sweeps; fixed dofs keep the input values [ref: multigrid.py:375-385]
+  cudaStream_t s = (cudaStream_t)stream;
+  if (l < 0 || l >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
+  vt_grid* G = H->lv[l];
+  const size_t bytes = G->vec_len() * sizeof(double);
+  VT_CUDA(cudaMemcpyAsync(out, u, bytes, cudaMemcpyDeviceToDevice, s));
+  for (int k = 0; k < sweeps; ++k) {
+    VT_TRY(launch_project(G, out, G->scratch, s));
+    VT_TRY(launch_hex8(G, H8_SMOOTH, false, H->scale[l], G->scratch, out, f, G->scratch2,
+                       H->omega, nullptr, nullptr, s));
+    VT_CUDA(cudaMemcpyAsync(out, G->scratch2, bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  return VT_OK;
+}
+
+vt_status vt_hier_level_apply(vt_hier* H, int l, const double* u, double* v, void* stream) {
+  if (l < 0 || l >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
+  return vt_apply(H->lv[l], H->scale[l], u, v, stream);
+}
+
+vt_status vt_hier_level_diag(vt_hier* H, int l, double* d, void* stream) {
+  if (l < 0 || l >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
+  return vt_diagonal(H->lv[l], H->scale[l], d, stream);
+}
+
+vt_status vt_hier_coarse_solve(vt_hier* H, const double* f, double* u, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!H->factored) return fail(VT_ESETUP, "hierarchy was not refreshed before use");
+  vt_grid* G = H->lv.back();
+  const size_t sm = (size_t)H->nL * sizeof(double);
+  coarse_solve_kernel<<<(H->nL + 255) / 256 > 32 ? 32 : (H->nL + 255) / 256, 256, sm, s>>>(
+      G->g, G->mask, H->nL, H->Kinv, f, u, nullptr);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+}  // extern "C"

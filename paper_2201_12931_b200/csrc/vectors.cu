@@ -1,0 +1,363 @@
+// Vector passes, deterministic reductions and the device-resident PCG scalar
+// logic [ref: solver.py:62-167].  All element-wise updates reproduce the
+// reference's numpy rounding (separate multiply and add, no contraction).
+#include <math.h>
+
+#include "vt_internal.h"
+#include "vt_pcg.cuh"
+
+namespace vt {
+
+constexpr int VT_THREADS = 256;
+
+int dot_grid(vt_grid* G) { return G->nsm * 4; }
+
+// owned region of a node vector: planes [pA, pB) are contiguous
+__device__ __forceinline__ void owned_range(const Geom& g, long long& b, long long& e) {
+  b = (long long)g.pA * g.nplane;
+  e = (long long)g.pB * g.nplane;
+}
+
+// ---------------------------------------------------------------- projection
+__global__ void project_kernel(Geom g, const uint8_t* mask, const double* src, double* dst) {
+  long long b, e;
+  owned_range(g, b, e);
+  const long long nn = (e - b) / 3;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long node = b / 3 + t;
+    const unsigned m = mask[node];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dst[node * 3 + c] = ((m >> c) & 1u) ? 0.0 : src[node * 3 + c];
+  }
+}
+
+vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_t s) {
+  project_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, G->mask, src, dst);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+__global__ void zero_owned_kernel(Geom g, double* v) {
+  long long b, e;
+  owned_range(g, b, e);
+  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = 0.0;
+}
+vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s) {
+  zero_owned_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, v);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// ---------------------------------------------------------------- dots
+__global__ void dot_kernel(Geom g, const double* __restrict__ x, const double* __restrict__ y,
+                           double* partial, const int* stop) {
+  __shared__ double red[VT_THREADS / 32];
+  if (stop && *(volatile const int*)stop) return;
+  long long b, e;
+  owned_range(g, b, e);
+  double acc = 0.0;
+  const double2* x2 = reinterpret_cast<const double2*>(x + b);
+  const double2* y2 = reinterpret_cast<const double2*>(y + b);
+  const long long n2 = (e - b) / 2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = x2[i], c = y2[i];
+    acc = fma(a.x, c.x, acc);
+    acc = fma(a.y, c.y, acc);
+  }
+  const double s = block_sum<VT_THREADS>(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+vt_status launch_dot(vt_grid* G, const double* x, const double* y, double* partial, int* nparts,
+                     cudaStream_t s, const int* stop) {
+  const int grid = dot_grid(G);
+  dot_kernel<<<grid, VT_THREADS, 0, s>>>(G->g, x, y, partial, stop);
+  count_launch();
+  if (nparts) *nparts = grid;
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+__global__ void sum_partials_kernel(const double* p, int n, double* out) {
+  const double s = warp_sum_partials(p, n);
+  if (threadIdx.x == 0) *out = s;
+}
+vt_status launch_sum_partials(const double* partial, int n, double* out, cudaStream_t s) {
+  sum_partials_kernel<<<1, 32, 0, s>>>(partial, n, out);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// ---------------------------------------------------------------- diagonal
+// d = K0_ii * sum over incident elements (corner order c = 0..7), 1 on fixed
+// [ref: operator.py:84-105].  Node plane p gets corners ck=0 from element
+// layer q=p and ck=1 from q=p-1 (local coords, see voxb200.h).
+__device__ __forceinline__ double node_diag(const Geom& g, const double* scale, int p, int j,
+                                            int i, double kd) {
+  double d = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int ei = i - (c & 1), ej = j - ((c >> 1) & 1), q = p - ((c >> 2) & 1);
+    const int k = q + g.k0 - 1;  // global element layer
+    if (ei < 0 || ei >= g.nx || ej < 0 || ej >= g.ny || q < 0 || q >= g.Q || k < 0 || k >= g.nz)
+      continue;
+    d = __dadd_rn(d, __dmul_rn(scale[elem_off(g, q, ej, ei)], kd));
+  }
+  return d;
+}
+
+__global__ void diag_kernel(Geom g, const uint8_t* mask, const double* scale, double kd,
+                            double* out) {
+  const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (g.nx + 1));
+    const long long r = t / (g.nx + 1);
+    const int j = (int)(r % (g.ny + 1));
+    const int p = (int)(r / (g.ny + 1)) + g.pA;
+    const long long node = node_off(g, p, j, i);
+    const double d = node_diag(g, scale, p, j, i, kd);
+    const unsigned m = mask[node];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[node * 3 + c] = ((m >> c) & 1u) ? 1.0 : d;
+  }
+}
+
+vt_status launch_diag(vt_grid* G, const double* scale, double* d, cudaStream_t s) {
+  diag_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, G->mask, scale, G->coef.kd, d);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// u = omega * (f / d) on free dofs, 0 on fixed: the first pre-smoothing sweep
+// from a zero iterate, bit-identical to the reference's
+// u += omega * ((f - K 0) / d) [ref: multigrid.py:387-393, 423-424].
+__global__ void jacobi0_kernel(Geom g, const uint8_t* mask, const double* scale, double kd,
+                               double omega, const double* f, double* u, const int* stop) {
+  if (stop && *(volatile const int*)stop) return;
+  const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (g.nx + 1));
+    const long long r = t / (g.nx + 1);
+    const int j = (int)(r % (g.ny + 1));
+    const int p = (int)(r / (g.ny + 1)) + g.pA;
+    const long long node = node_off(g, p, j, i);
+    const unsigned m = mask[node];
+    const double d = node_diag(g, scale, p, j, i, kd);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      u[node * 3 + c] = ((m >> c) & 1u) ? 0.0 : __dmul_rn(omega, __ddiv_rn(f[node * 3 + c], d));
+  }
+}
+
+vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const double* f,
+                         double* u, const int* stop, cudaStream_t s) {
+  jacobi0_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, G->mask, scale, G->coef.kd, omega, f, u,
+                                                   stop);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// ---------------------------------------------------------------- PCG passes
+// x += alpha p ; r -= alpha q ; partial ||r||^2   [ref: solver.py:131-136]
+__global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict__ x,
+                                  const double* __restrict__ p, double* __restrict__ r,
+                                  const double* __restrict__ q, double* partial, int with_r) {
+  __shared__ double red[VT_THREADS / 32];
+  const int skip = with_r ? ctl->skip_rec : ctl->skip_true50;
+  if (skip) return;
+  const double alpha = ctl->alpha;
+  long long b, e;
+  owned_range(g, b, e);
+  double acc = 0.0;
+  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    if (with_r) {
+      const double rv = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+      r[i] = rv;
+      acc = fma(rv, rv, acc);
+    }
+  }
+  if (with_r) {
+    const double s = block_sum<VT_THREADS>(acc, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  }
+}
+
+// p = z + beta p   [ref: solver.py:158]
+__global__ void pcg_xpby_kernel(Geom g, const PcgCtl* ctl, const double* __restrict__ z,
+                                double* __restrict__ p) {
+  if (ctl->stop) return;
+  const double beta = ctl->beta;
+  long long b, e;
+  owned_range(g, b, e);
+  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
+// conditional copy dst = src (skip flag)
+__global__ void copy_kernel(Geom g, const int* skip, const double* __restrict__ src,
+                            double* __restrict__ dst) {
+  if (skip && *(volatile const int*)skip) return;
+  long long b, e;
+  owned_range(g, b, e);
+  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// z = r / d (+ partial r.z) -- Jacobi preconditioner [ref: solver.py:57-59]
+__global__ void jacobi_precond_kernel(Geom g, const int* stop, const double* __restrict__ r,
+                                      const double* __restrict__ d, double* __restrict__ z,
+                                      double* partial) {
+  __shared__ double red[VT_THREADS / 32];
+  if (stop && *(volatile const int*)stop) return;
+  long long b, e;
+  owned_range(g, b, e);
+  double acc = 0.0;
+  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double rv = r[i];
+    // pad entries carry d = 0 -> treat as 0/1
+    const double dv = d[i];
+    const double zv = dv != 0.0 ? __ddiv_rn(rv, dv) : 0.0;
+    z[i] = zv;
+    acc = fma(rv, zv, acc);
+  }
+  const double s = block_sum<VT_THREADS>(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// ---------------------------------------------------------------- scalar steps
+// S1: pq -> alpha, iteration counter, curvature checks [ref: solver.py:121-132]
+__global__ void pcg_s1_kernel(PcgCtl* c, const double* partial, int n) {
+  if (c->stop) return;
+  const double pq = warp_sum_partials(partial, n);
+  if (threadIdx.x != 0) return;
+  c->k += 1;
+  c->pq = pq;
+  if (!isfinite(pq)) {
+    c->err = 2; c->err_iter = c->k; c->err_val = pq; c->stop = 1;
+  } else if (pq <= 0.0) {
+    c->err = 3; c->err_iter = c->k; c->err_val = pq; c->stop = 1;
+  }
+  const int stop = c->stop;
+  c->alpha = c->rz / pq;
+  const int is50 = (c->k % 50) == 0;
+  c->skip_rec = stop || is50;
+  c->skip_true50 = stop || !is50;
+  c->skip_cand = 1;
+  c->skip_swap = 1;
+}
+
+// S2: rel = ||r|| / ||f|| ; candidate convergence [ref: solver.py:137-140]
+__global__ void pcg_s2_kernel(PcgCtl* c, const double* partial, int n_rec, int n_true) {
+  if (c->stop) return;
+  const int is50 = (c->k % 50) == 0;
+  const double rr = warp_sum_partials(partial, is50 ? n_true : n_rec);
+  if (threadIdx.x != 0) return;
+  const double rel = sqrt(rr) / c->fnorm;
+  c->rel = rel;
+  if (!isfinite(rel)) {
+    c->err = 4; c->err_iter = c->k; c->err_val = rel; c->stop = 1;
+    return;
+  }
+  c->skip_cand = !(rel <= c->tol);
+}
+
+// S3: true residual check on a convergence candidate [ref: solver.py:140-149]
+__global__ void pcg_s3_kernel(PcgCtl* c, const double* partial, int n) {
+  if (c->skip_cand || c->stop) return;
+  const double tr = warp_sum_partials(partial, n);
+  if (threadIdx.x != 0) return;
+  const double trel = sqrt(tr) / c->fnorm;
+  c->drift = fabs(trel - c->rel) / fmax(trel, 1e-300);
+  c->rel = trel;
+  if (trel <= c->tol) {
+    c->converged = 1;
+    c->stop = 1;
+  } else {
+    c->skip_swap = 0;
+  }
+}
+
+// S4: r.z -> beta [ref: solver.py:150-159]
+__global__ void pcg_s4_kernel(PcgCtl* c, const double* partial, int n, int counts) {
+  if (c->stop) return;
+  const double rz = warp_sum_partials(partial, n);
+  if (threadIdx.x != 0) return;
+  if (counts) c->precond_apps += 1;
+  if (!isfinite(rz) || rz <= 0.0) {
+    c->err = 1; c->err_iter = c->k; c->err_val = rz; c->stop = 1;
+    return;
+  }
+  c->beta = rz / c->rz;
+  c->rz = rz;
+}
+
+vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p, double* r,
+                            const double* q, double* partial, int with_r, cudaStream_t s) {
+  pcg_update_kernel<<<dot_grid(G), VT_THREADS, 0, s>>>(G->g, ctl, x, p, r, q, partial, with_r);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s) {
+  pcg_xpby_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, ctl, z, p);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+vt_status launch_copy(vt_grid* G, const int* skip, const double* src, double* dst,
+                      cudaStream_t s) {
+  copy_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, skip, src, dst);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+vt_status launch_jacobi_precond(vt_grid* G, const int* stop, const double* r, const double* d,
+                                double* z, double* partial, cudaStream_t s) {
+  jacobi_precond_kernel<<<dot_grid(G), VT_THREADS, 0, s>>>(G->g, stop, r, d, z, partial);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+vt_status launch_pcg_s1(PcgCtl* c, const double* partial, int n, cudaStream_t s) {
+  pcg_s1_kernel<<<1, 32, 0, s>>>(c, partial, n);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+vt_status launch_pcg_s2(PcgCtl* c, const double* partial, int n_rec, int n_true,
+                        cudaStream_t s) {
+  pcg_s2_kernel<<<1, 32, 0, s>>>(c, partial, n_rec, n_true);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+vt_status launch_pcg_s3(PcgCtl* c, const double* partial, int n, cudaStream_t s) {
+  pcg_s3_kernel<<<1, 32, 0, s>>>(c, partial, n);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+vt_status launch_pcg_s4(PcgCtl* c, const double* partial, int n, int counts, cudaStream_t s) {
+  pcg_s4_kernel<<<1, 32, 0, s>>>(c, partial, n, counts);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+}  // namespace vt

@@ -1,0 +1,102 @@
+// Host-side runtime structures of libvoxb200 (not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/voxb200.h"
+#include "vt_device.cuh"
+
+namespace vt {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+vt_status fail(vt_status code, const std::string& msg);
+vt_status cuda_fail(cudaError_t e, const char* what);
+#define VT_CUDA(call)                                     \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return ::vt::cuda_fail(e_, #call); \
+  } while (0)
+#define VT_TRY(call)                  \
+  do {                                \
+    vt_status s_ = (call);            \
+    if (s_ != VT_OK) return s_;       \
+  } while (0)
+
+extern unsigned long long g_launches;  // kernels launched by this library
+inline void count_launch(int n = 1) { g_launches += (unsigned long long)n; }
+
+// Element-operator constants of one level (factorized hex8):
+// kc = h*{lam/16, mu/8, mu/16, lam/48, mu/48, lam/144+mu/36}, kd = K0 diagonal.
+struct Hex8Coef {
+  double kc[6];
+  double kd;
+};
+Hex8Coef hex8_coef(double nu, double h);
+
+// Apply-family kernel modes.
+enum Hex8Mode { H8_APPLY = 0, H8_RESID = 1, H8_SMOOTH = 2 };
+
+struct Hex8Launch {
+  int grid;        // persistent CTAs
+  int tiles_x, tiles_y;
+  long long work;  // tiles_x * tiles_y * owned planes
+};
+
+}  // namespace vt
+
+// ------------------------------------------------------------------- grid
+struct vt_grid {
+  int device = 0;
+  vt::Geom g{};
+  double h = 1.0, nu = 0.3;
+  vt::Hex8Coef coef{};
+  uint8_t* mask = nullptr;          // node layout (P planes), 1 byte per node
+  long long n_fixed = 0;
+  double* partial = nullptr;        // reduction partials (>= 4096 doubles)
+  double* scalars = nullptr;        // small device scalar scratch (64 doubles)
+  double* host_scalars = nullptr;   // pinned mirror
+  double* scratch = nullptr;        // one node vector (projected inputs)
+  double* scratch2 = nullptr;       // a second node vector
+  vt::Hex8Launch h8{};
+  int nsm = 148;
+  std::map<const void*, CUtensorMap> vec_maps;   // node-vector TMA descriptors
+  std::map<const void*, CUtensorMap> elem_maps;  // element-field TMA descriptors
+  // PCG workspace (lazily allocated)
+  double *w_x = nullptr, *w_f = nullptr, *w_r = nullptr, *w_p = nullptr, *w_q = nullptr,
+         *w_z = nullptr, *w_t = nullptr, *w_d = nullptr;
+  void* pcg_ctl = nullptr;          // device control block
+  void* pcg_ctl_host = nullptr;     // pinned mirror (ring of 2)
+  cudaGraphExec_t pcg_graph = nullptr;
+  const void* pcg_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  unsigned long long pcg_nodes = 0;   // kernel nodes per PCG iteration graph
+
+  long long vec_len() const { return (long long)g.P * g.nplane; }
+  long long elem_len() const { return (long long)g.Q * g.eplane; }
+  long long nel_local() const { return (long long)g.nx * g.ny * (g.k1 - g.k0); }
+};
+
+namespace vt {
+// TMA descriptors (cached per device pointer)
+const CUtensorMap* vec_map(vt_grid* G, const void* ptr);
+const CUtensorMap* elem_map(vt_grid* G, const void* ptr);
+
+// kernel launchers (hex8_apply.cu)
+Hex8Launch hex8_plan(const Geom& g, int nsm);
+vt_status hex8_configure();
+vt_status launch_hex8(vt_grid* G, int mode, bool dot, const double* scale, const double* u,
+                      const double* ufix, const double* f, double* out, double omega,
+                      double* partial, const int* stop, cudaStream_t s);
+// (vectors.cu)
+vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_t s);
+vt_status launch_dot(vt_grid* G, const double* x, const double* y, double* partial, int* nparts,
+                     cudaStream_t s, const int* stop = nullptr);
+vt_status launch_sum_partials(const double* partial, int n, double* out, cudaStream_t s);
+vt_status launch_diag(vt_grid* G, const double* scale, double* d, cudaStream_t s);
+vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s);
+int dot_grid(vt_grid* G);
+}  // namespace vt

@@ -1,0 +1,185 @@
+"""MGPCG / PCG and design-loop parity on the GPU against the reference goldens
+(mirrors pkg/tests/test_solver.py, test_optimize.py, test_acceptance.py)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, face_fixed_mask, golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+vb = pytest.importorskip("paper_2201_12931_b200")
+from oracle import cpu_path as O  # noqa: E402
+
+
+def _cantilever(nx, ny, nz, gravity=None):
+    case = O.cantilever_case(nx, ny, nz, gravity=gravity)
+    grid = vb.build_grid(nx, ny, nz, case.h)
+    fixed = np.flatnonzero(case.fixed_mask)
+    loads = [(int(d), float(case.f_ext[d])) for d in np.flatnonzero(case.f_ext)]
+    gs = None if gravity is None else vb.GravitySpec(*gravity)
+    bnd = vb.make_boundary(grid, fixed, loads, gs)
+    return case, grid, vb.Problem(grid, bnd, vb.classify_regions(grid, []))
+
+
+@pytest.mark.parametrize("tag", ["u", "r"])
+def test_mgcg_matches_reference(tag):
+    g = golden("pcg.npz")
+    case, grid, _ = _cantilever(16, 8, 8)
+    st = vb.OperatorState(grid, g[f"{tag}_rho"], vb.MaterialModel(), case.fixed_mask)
+    H = vb.build_hierarchy(grid, st, 3, scheme="homogenized")
+    f = g["f"]
+    for ctag, tol, maxit in (("a", 1e-5, 200), ("b", 1e-10, 500), ("c", 1e-12, 3), ("d", 1e-8, 120)):
+        u0 = g[f"{tag}{ctag}_u0"] if ctag == "d" else None
+        x, rep = vb.mgcg_solve(st, H, f, u_prev=u0, cfg=vb.SolverConfig(tolerance=tol, max_iterations=maxit))
+        want = g[f"{tag}{ctag}_rep"]
+        assert rep.iterations == int(want[0]), (ctag, rep)
+        assert rep.precond_applications == int(want[2])
+        assert rep.converged == bool(want[3])
+        assert rep.aux_vector_scalars == int(want[4])
+        assert abs(rep.final_rel_residual - want[1]) <= 1e-6 * want[1] + 1e-15
+        assert rel_err(x, g[f"{tag}{ctag}_x"]) <= 1e-8
+
+
+@pytest.mark.parametrize("tag", ["u", "r"])
+def test_jacobi_and_plain_cg_match_reference(tag):
+    g = golden("pcg.npz")
+    case, grid, _ = _cantilever(16, 8, 8)
+    st = vb.OperatorState(grid, g[f"{tag}_rho"], vb.MaterialModel(), case.fixed_mask)
+    cfg = vb.SolverConfig(tolerance=1e-8, max_iterations=2000)
+    for key, pre in (("j", vb.jacobi_preconditioner(st)), ("n", None)):
+        x, rep = vb.pcg(st, pre, g["f"], cfg=cfg)
+        want = g[f"{tag}{key}_rep"]
+        # long unpreconditioned runs may drift by an iteration at the tolerance boundary
+        assert abs(rep.iterations - int(want[0])) <= max(1, int(0.01 * want[0])), (key, rep.iterations, want)
+        assert rep.converged == bool(want[3])
+        assert rel_err(x, g[f"{tag}{key}_x"]) <= 1e-6
+
+
+def test_pcg_breakdown_and_zero_rhs(rng):
+    case, grid, _ = _cantilever(8, 4, 4)
+    st = vb.OperatorState(grid, np.full(grid.n_elements, 0.5), vb.MaterialModel(), case.fixed_mask)
+    x, rep = vb.pcg(st, None, np.zeros(grid.n_dofs), u0=rng.standard_normal(grid.n_dofs))
+    assert rep.converged and rep.iterations == 0
+    assert np.all(x[st.fixed_idx] == 0.0)
+    with pytest.raises(vb.SolverBreakdown, match="SPD"):
+        vb.pcg(st, lambda r: -r, case.f_ext * (~case.fixed_mask))
+    bad = np.zeros(grid.n_dofs)
+    bad[5] = np.nan
+    with pytest.raises(vb.SolverBreakdown):
+        vb.pcg(st, None, bad)
+    f = case.f_ext * (~case.fixed_mask)
+    x, rep = vb.pcg(st, None, f, cfg=vb.SolverConfig(tolerance=1e-12, max_iterations=3))
+    assert not rep.converged and rep.iterations == 3
+
+
+def test_design_kernels_match_reference():
+    g = golden("design.npz")
+    grid = vb.build_grid(12, 6, 5, 0.75)
+    st = vb.OperatorState(grid, g["rho"], vb.MaterialModel(), face_fixed_mask(12, 6, 5),
+                          vb.unit_stiffness(0.3, 0.75))
+    assert rel_err(vb.sensitivities(st, g["u"]), g["dc"]) <= 1e-12
+    grav = vb.GravitySpec(axis=2, g=9.81, unit_weight=0.7)
+    assert rel_err(vb.sensitivities(st, g["u"], grav), g["dcg"]) <= 1e-12
+    regions = vb.classify_regions(grid, [])
+    fld = vb.DensityField(g["rho"], regions)
+    assert np.array_equal(vb.update_gravity_load(grid, fld, grav, g["f_ext"], st.fixed_idx), g["fgrav"])
+    assert np.array_equal(vb.update_gravity_load(grid, fld, grav), g["fgrav_plain"])
+    for tag, r in (("r15", 1.5 * 0.75), ("r25", 2.5 * 0.75), ("r18", 1.8 * 0.75)):
+        w = vb.build_filter(grid, r)
+        assert np.array_equal(w.kernel, g[f"{tag}_kernel"])
+        assert np.array_equal(w.wsum, g[f"{tag}_wsum"])
+        out = vb.filter_sensitivities(g["dcin"], g["rho"], w, 1e-3)
+        assert np.array_equal(out, g[f"{tag}_dcf"])
+    reg = vb.RegionMask(g["oc_classes"])
+    for tag, kw in (("a", dict(volfrac=0.3)), ("b", dict(volfrac=0.3, move=0.1, q=2.0)), ("c", dict(volfrac=0.25, eta=0.3))):
+        res = vb.oc_update(vb.DensityField(g["oc_x0"], reg), g["dcin"], np.ones(grid.n_elements),
+                           vb.OptConfig(filter_radius=1.0, **kw))
+        assert res.bisection_steps == int(g[f"oc{tag}_steps"])
+        assert abs(res.lam - float(g[f"oc{tag}_lam"])) <= 1e-12 * abs(float(g[f"oc{tag}_lam"]))
+        assert np.abs(res.densities.values - g[f"oc{tag}_rho"]).max() <= 1e-12
+
+
+def test_oc_infeasible_raises():
+    grid = vb.build_grid(2, 2, 2, 1.0)
+    rho = vb.DensityField(np.full(8, 0.1), vb.classify_regions(grid, []))
+    with pytest.raises(vb.VolumeInfeasible):
+        vb.oc_update(rho, -np.ones(8), np.ones(8), vb.OptConfig(volfrac=0.9, filter_radius=1.0, move=0.1))
+
+
+def _traj_check(res, want, rho_ref, c_tol=1e-9, rho_tol=1e-6):
+    recs = res.records
+    assert len(recs) == want.shape[0]
+    for r, w in zip(recs, want):
+        assert r.iteration == int(w[0])
+        assert r.cg_iters == int(w[4]), (r.iteration, r.cg_iters, w[4])
+        assert abs(r.compliance - w[1]) <= c_tol * abs(w[1]), (r.iteration, r.compliance, w[1])
+        assert abs(r.volume - w[2]) <= 1e-9
+        assert r.aux_scalars == int(w[6])
+    assert np.abs(res.densities.values - rho_ref).max() <= rho_tol
+
+
+def test_small_trajectory_matches_reference():
+    g = golden("small_traj.npz")
+    case, grid, prob = _cantilever(16, 8, 8)
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=2.5 * grid.h, max_iterations=30, ch_tol=1e-12)
+    res = vb.run(prob, opt, vb.SolverConfig(tolerance=1e-5), scheme="homogenized", max_levels=3)
+    _traj_check(res, g["recs"], g["rho30"], c_tol=1e-8, rho_tol=1e-5)
+
+
+def test_bridge_trajectory_matches_reference():
+    g = golden("bridge_traj.npz")
+    case = O.bridge_case(32, 16, 16)
+    grid = vb.build_grid(32, 16, 16, case.h)
+    loads = [(int(d), float(case.f_ext[d])) for d in np.flatnonzero(case.f_ext)]
+    bnd = vb.make_boundary(grid, np.flatnonzero(case.fixed_mask), loads)
+    Lx, Ly, Lz = grid.domain
+    reg = vb.classify_regions(grid, [(vb.Box((0, 0, Lz - grid.h), (Lx, Ly, Lz)), vb.Region.PASSIVE_SOLID)])
+    assert np.array_equal(reg.classes, case.classes)
+    opt = vb.OptConfig(volfrac=0.14, filter_radius=1.5 * grid.h, max_iterations=3, ch_tol=1e-12)
+    res = vb.run(vb.Problem(grid, bnd, reg), opt, vb.SolverConfig(tolerance=1e-5), scheme="homogenized")
+    _traj_check(res, g["recs"], g["rho3"])
+
+
+def test_gravity_trajectory_and_failure():
+    g = golden("grav_traj.npz")
+    case, grid, prob = _cantilever(32, 16, 16, gravity=(2, 1.0, 1e-3))
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * grid.h, max_iterations=4, ch_tol=1e-12)
+    res = vb.run(prob, opt, vb.SolverConfig(tolerance=1e-5), scheme="homogenized")
+    _traj_check(res, g["recs"], g["rho4"])
+    info = json.load(open(os.path.join(GOLDEN, "grav_fail.json")))
+    case, grid, prob = _cantilever(32, 16, 16, gravity=(2, 1.0, 1.0))
+    seen = []
+    with pytest.raises(vb.VolumeInfeasible):
+        vb.run(prob, opt, vb.SolverConfig(tolerance=1e-5), scheme="homogenized",
+               on_iteration=lambda r, a, b: seen.append(r.compliance))
+    assert info["raised"] == "VolumeInfeasible"
+    assert len(seen) == len(info["compliance"])
+    assert abs(seen[0] - info["compliance"][0]) <= 1e-9 * abs(seen[0])
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "cfg1_traj.npz")), reason="cfg1 fixture missing")
+def test_cfg1_trajectory_parity():
+    """BASELINE config 1: 48x24x24 cantilever, p=3, rmin=1.5h, 4-level homogenized MG,
+    40 SIMP iterations; north-star bars: compliance <= 1e-6 rel, rho <= 1e-4 max-abs."""
+    g = golden("cfg1_traj.npz")
+    case, grid, prob = _cantilever(48, 24, 24)
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * grid.h, p=3.0, max_iterations=40, ch_tol=1e-12)
+    seen = {}
+
+    def hook(rec, rho, u):
+        if rec.iteration in (20, 40):
+            seen[rec.iteration] = rho.values.copy()
+
+    res = vb.run(prob, opt, vb.SolverConfig(tolerance=1e-5), scheme="homogenized", max_levels=4,
+                 on_iteration=hook)
+    want = g["recs"]
+    worst_c = max(abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(res.records, want))
+    same_its = sum(int(r.cg_iters == int(w[4])) for r, w in zip(res.records, want))
+    print(f"cfg1: worst compliance rel diff {worst_c:.2e}, equal CG counts {same_its}/40")
+    assert worst_c <= 1e-6
+    assert np.abs(seen[20] - g["rho20"]).max() <= 1e-4
+    assert np.abs(seen[40] - g["rho40"]).max() <= 1e-4
