@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark: matvec GDOF/s (HBM roofline) and MGPCG solve s per SIMP iteration.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config cfg2]
+
+Metric (BASELINE.json): "MGPCG solve s per SIMP iter & matvec GDOF/s at 1/2/4/8
+B200 (HBM roofline %)".  `value` is the whole-job matvec throughput (GDOF/s)
+of the matrix-free hex8 operator on the configuration BASELINE quotes for one
+B200 (cfg2, cantilever 256x128x128, 12.8M dofs): one step = one application
+of K(rho) to a device-resident vector, the operator CG applies every
+iteration.  The MGPCG solve time per SIMP iteration of the same problem is
+reported beside it ("solve"), from real SIMP iterations of the design loop.
+`e2e` is the same metric through the public Python API with host numpy
+buffers (H2D + kernel + D2H inside the timed region).
+
+Under torchrun (N > 1) every rank runs its own cfg2 replica (weak scaling);
+the z-slab decomposition with NCCL halos is the next step.
+--impl reference times the reference algorithm's CPU implementation (the
+numpy oracle restatement, oracle/cpu_path.py) on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MGPCG solve s per SIMP iter & matvec GDOF/s at 1/2/4/8 B200 (HBM roofline %)"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--simp-iters", type=int, default=4, help="SIMP iterations timed for the solve figure")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    return ap.parse_args()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------- ours
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2201_12931_b200 as vb
+    from paper_2201_12931_b200 import cases
+    from paper_2201_12931_b200._lib import lib
+    from paper_2201_12931_b200.design import DeviceRun
+    from paper_2201_12931_b200.device import ptr, stream_ptr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    spec = cases.CONFIGS[a.config]
+    nx, ny, nz = spec["dims"]
+    problem = spec["builder"](nx, ny, nz)
+    grid = problem.grid
+    n, nel = grid.n_dofs, grid.n_elements
+    rng = np.random.default_rng(0)
+    rho = rng.uniform(0.0, 1.0, nel)
+    fm = problem.boundary.fixed_mask(grid)
+    state = vb.OperatorState(grid, rho, problem.model, fm, problem.stiffness())
+    d = state.dgrid
+    u_host = rng.standard_normal(n)
+    u_host[fm] = 0.0
+    u = d.upload(u_host)
+    v = d.zeros()
+    stream = torch.cuda.current_stream()
+    sp = stream_ptr()
+
+    def step():
+        lib.vt_apply_projected(d.handle, ptr(state.scale_dev), ptr(u), ptr(v), sp)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    barrier()
+    l0 = vb.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+    launches = vb.launch_count() - l0
+    t_step = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / a.steps)
+    gdofs = world * n / t_step / 1e9
+    alg_bytes = 16.0 * n + 8.0 * nel  # read u, write v (8 B/dof each) + read scale (8 B/element)
+    hbm_peak, peak_src = _peaks()
+    achieved = alg_bytes / t_step / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: public API, host numpy in -> numpy out (pinned host buffers)
+    pin_u = torch.from_numpy(u_host).pin_memory()
+    u_np = pin_u.numpy()
+    for _ in range(2):
+        vb.apply(state, u_np)
+    torch.cuda.synchronize()
+    ke = max(3, a.steps // 4)
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        out = vb.apply(state, u_np)
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks((time.perf_counter() - t0) / ke)
+    assert out.shape == (n,)
+
+    # ---- MGPCG solve per SIMP iteration (real design iterations of the same problem)
+    solve = None
+    if a.simp_iters > 0:
+        opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
+        R = DeviceRun(problem, opt, vb.SolverConfig(tolerance=1e-5), "homogenized", spec["levels"], 0.4)
+        times, its = [], []
+        for it in range(a.simp_iters):
+            model = problem.model
+            barrier()
+            ts = time.perf_counter()
+            rep = R.solve(model)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - ts)
+            its.append(rep.iterations)
+            R.design_step(model)
+        barrier()
+        ts_mean = max_over_ranks(sum(times) / len(times))
+        solve = {"s_per_simp_iter": ts_mean, "simp_iters": a.simp_iters, "cg_iters": its,
+                 "ms_per_cg_iter": 1e3 * sum(times) / max(1, sum(its)), "levels": R.hier.n_levels,
+                 "note": "first SIMP iterations of the cfg design loop (homogenized MG, V(1,1), tol 1e-5)"}
+
+    res = {
+        "metric": METRIC,
+        "value": gdofs,
+        "unit": "GDOF/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (rho ~ U(0,1), u ~ N(0,1), seed 0)",
+        "config": {"workload": f"{a.config} cantilever {nx}x{ny}x{nz} hex8 matrix-free K(rho)u, "
+                               f"{n} dofs, {nel} elements", "dofs": n, "elements": nel,
+                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU",
+                   "l2": "inputs larger than L2 (apply working set %.0f MB > 126 MB)" % (alg_bytes / 1e6)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "e2e": {"value": world * n / t_e2e / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "solve": solve,
+    }
+    if rank == 0 and world == 1 and not a.no_cpu:
+        res["cpu_baseline"] = cpu_baseline(a.config, reps=2)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(res))
+
+
+# ---------------------------------------------------------------------- CPU baseline
+def _oracle_apply_setup(config):
+    import numpy as np
+
+    from oracle import cpu_path as O  # CPU baseline leg only
+
+    from paper_2201_12931_b200.cases import CONFIGS
+
+    nx, ny, nz = CONFIGS[config]["dims"]
+    case = O.cantilever_case(nx, ny, nz)
+    rng = np.random.default_rng(0)
+    rho = rng.uniform(0.0, 1.0, nx * ny * nz)
+    scale = O.simp(rho, 3.0, 1e-9)
+    u = rng.standard_normal(case.fixed_mask.size)
+    fixed = np.flatnonzero(case.fixed_mask)
+    u[fixed] = 0.0
+    k0 = O.hex8_k0(0.3, case.h)
+    return lambda: O.apply_k(u, case.es, fixed, k0, scale), u.size
+
+
+def cpu_baseline(config, reps=2):
+    fn, n = _oracle_apply_setup(config)
+    fn()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": n / dt / 1e9, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{reps} applications of the numpy oracle K(rho)u on the full {config} grid "
+                      f"({dt:.2f} s each, OpenBLAS threads = all host cores)"}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    fn, n = _oracle_apply_setup(a.config)
+    for _ in range(a.warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        fn()
+    dt = (time.perf_counter() - t0) / a.steps
+    v = n / dt / 1e9
+    cores = os.cpu_count()
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GDOF/s", "n_gpus": 0,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (rho ~ U(0,1), u ~ N(0,1), seed 0)",
+        "config": {"workload": f"{a.config} cantilever, reference CPU K(rho)u (numpy oracle port)"},
+        "cpu_baseline": {"value": v, "unit": "GDOF/s", "cores": cores, "kind": "port",
+                         "sample": f"{a.steps} timed applications on the full {a.config} grid"},
+        "e2e": {"value": v, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

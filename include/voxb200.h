@@ -97,6 +97,10 @@ vt_status vt_scale_from_density(vt_grid *g, const double *rho, double p, double 
  * v = K(rho) u with identity on fixed dofs; u is projected to zero on fixed
  * dofs before the product [ref: operator.py:58-81, 154-165]. */
 vt_status vt_apply(vt_grid *g, const double *scale, const double *u, double *v, void *stream);
+/* Solver-internal apply: u must already be zero on fixed dofs (every CG /
+ * multigrid vector is); skips the projection pass of vt_apply. */
+vt_status vt_apply_projected(vt_grid *g, const double *scale, const double *u, double *v,
+                             void *stream);
 /* d = diag K, 1 on fixed [ref: operator.py:84-105, 168-174] */
 vt_status vt_diagonal(vt_grid *g, const double *scale, double *d, void *stream);
 /* r = f - K u, zero on fixed [ref: operator.py:177-184] */

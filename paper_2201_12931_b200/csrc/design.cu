@@ -126,7 +126,7 @@ __global__ void gravity_kernel(Geom g, const uint8_t* mask, const double* __rest
       acc = __dadd_rn(acc, __dmul_rn(rho[e], gcoef));
     }
     const long long node = node_off(g, p, j, i);
-    const unsigned m = mask[node];
+    const unsigned m = mask[mask_off(g, p, j, i)];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       double v = (c == gax) ? acc : 0.0;

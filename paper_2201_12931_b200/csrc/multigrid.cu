@@ -101,7 +101,7 @@ __global__ void coarsen_mask_kernel(Geom gf, Geom gc, const uint8_t* mf, uint8_t
     node_coords(gc, t, p, j, i);
     const int K = p - 1 + gc.k0;
     const int pf = 2 * K - gf.k0 + 1;
-    mc[node_off(gc, p, j, i)] = mf[node_off(gf, pf, 2 * j, 2 * i)];
+    mc[mask_off(gc, p, j, i)] = mf[mask_off(gf, pf, 2 * j, 2 * i)];
   }
 }
 
@@ -112,7 +112,7 @@ __global__ void count_fixed_kernel(Geom g, const uint8_t* m, unsigned long long*
        t += (long long)gridDim.x * blockDim.x) {
     int p, j, i;
     node_coords(g, t, p, j, i);
-    c += __popc((unsigned)m[node_off(g, p, j, i)] & 7u);
+    c += __popc((unsigned)m[mask_off(g, p, j, i)] & 7u);
   }
   atomicAdd(out, c);  // integer: order-independent
 }
@@ -130,7 +130,7 @@ __global__ void restrict_kernel(Geom gf, Geom gc, const uint8_t* mc, const doubl
     node_coords(gc, t, p, J, I);
     const int K = p - 1 + gc.k0;
     const long long cnode = node_off(gc, p, J, I);
-    const unsigned m = mc[cnode];
+    const unsigned m = mc[mask_off(gc, p, J, I)];
     double out[3];
     // y/x neighbourhood of fine node (2J, 2I); index 0 = centre, 1 = +1, 2 = -1
     const int fj[3] = {2 * J, 2 * J + 1, 2 * J - 1};
@@ -192,7 +192,7 @@ __global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double
     node_coords(gf, t, p, j, i);
     const int k = p - 1 + gf.k0;
     const long long fnode = node_off(gf, p, j, i);
-    const unsigned m = mf[fnode];
+    const unsigned m = mf[mask_off(gf, p, j, i)];
     const int kz0 = k >> 1, kz1 = (k + 1) >> 1;
     const int jy0 = j >> 1, jy1 = (j + 1) >> 1;
     const int ix0 = i >> 1, ix1 = (i + 1) >> 1;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(1024, 1)
   for (int d = threadIdx.x; d < n; d += blockDim.x) {
     const int node = d / 3, c = d % 3;
     const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
-    if ((mask[node_off(g, k + 1, j, i)] >> c) & 1u) {
+    if ((mask[mask_off(g, k + 1, j, i)] >> c) & 1u) {
       for (int e = 0; e < n; ++e) A[(long long)d * n + e] = 0.0;
     }
   }
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(1024, 1)
     for (int e = 0; e < n; ++e) {
       const int node = e / 3, c = e % 3;
       const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
-      if ((mask[node_off(g, k + 1, j, i)] >> c) & 1u) A[(long long)d * n + e] = (d == e) ? 1.0 : 0.0;
+      if ((mask[mask_off(g, k + 1, j, i)] >> c) & 1u) A[(long long)d * n + e] = (d == e) ? 1.0 : 0.0;
     }
   }
   __syncthreads();
@@ -337,7 +337,7 @@ __global__ void coarse_solve_kernel(Geom g, const uint8_t* mask, int n, const do
       const int node = r / 3, c = r % 3;
       const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
       const long long nd = node_off(g, k + 1, j, i);
-      u[nd * 3 + c] = ((mask[nd] >> c) & 1u) ? 0.0 : s;
+      u[nd * 3 + c] = ((mask[mask_off(g, k + 1, j, i)] >> c) & 1u) ? 0.0 : s;
     }
   }
 }

@@ -130,7 +130,7 @@ const CUtensorMap* elem_map(vt_grid* G, const void* ptr) {
   if (it != G->elem_maps.end()) return &it->second;
   CUtensorMap m;
   const Geom& g = G->g;
-  if (!encode3d(&m, ptr, g.nx, g.ny, g.Q, 8ull * g.ep, 8ull * g.ep * g.ny, 32, 16)) return nullptr;
+  if (!encode3d(&m, ptr, g.nx, g.ny, g.Q, 8ull * g.ep, 8ull * g.ep * g.ny, 34, 16)) return nullptr;  // 32 + even-alignment slack
   if (G->elem_maps.size() > 256) G->elem_maps.clear();
   return &(G->elem_maps[ptr] = m);
 }
@@ -193,7 +193,8 @@ vt_status vt_grid_create(vt_grid** out, int nx, int ny, int nz, double h, double
   g.pA = 1;
   g.pB = k1 - k0 + 1 + g.last;
   g.nplane = (long long)(ny + 1) * g.rp * 3;
-  g.mplane = (long long)(ny + 1) * g.rp;
+  g.mp = ((nx + 1 + 15) / 16) * 16;
+  g.mplane = (long long)(ny + 1) * g.mp;
   g.eplane = (long long)ny * g.ep;
   G->coef = hex8_coef(nu, h);
   VT_CUDA(cudaDeviceGetAttribute(&G->nsm, cudaDevAttrMultiProcessorCount, device));
@@ -204,7 +205,7 @@ vt_status vt_grid_create(vt_grid** out, int nx, int ny, int nz, double h, double
   if (node_mask) {
     const int nown = g.pB - g.pA;
     const size_t row = (size_t)nx + 1;
-    VT_CUDA(cudaMemcpy2D(G->mask + (size_t)g.pA * g.mplane, g.rp,
+    VT_CUDA(cudaMemcpy2D(G->mask + (size_t)g.pA * g.mplane, g.mp,
                          node_mask + (size_t)k0 * (ny + 1) * row, row, row,
                          (size_t)nown * (ny + 1), cudaMemcpyHostToDevice));
     long long nf = 0;
@@ -219,6 +220,18 @@ vt_status vt_grid_create(vt_grid** out, int nx, int ny, int nz, double h, double
   VT_CUDA(cudaMallocHost(&G->host_scalars, 64 * sizeof(double)));
   VT_TRY(alloc_vec(G, &G->scratch));
   VT_TRY(alloc_vec(G, &G->scratch2));
+  // fixed-dof mask tiles travel with the TMA pipeline of the hex8 kernel
+  {
+    auto fn = encode_fn();
+    if (!fn) return fail(VT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)nx + 1, (cuuint64_t)ny + 1, (cuuint64_t)g.P};
+    cuuint64_t strides[2] = {(cuuint64_t)g.mp, (cuuint64_t)g.mplane};
+    cuuint32_t box[3] = {48, 16, 1}, es[3] = {1, 1, 1};
+    if (fn(&G->mask_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, G->mask, dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(VT_ECUDA, "mask tensor map encoding failed");
+  }
   *out = G;
   return VT_OK;
 }
@@ -227,6 +240,7 @@ vt_status vt_grid_destroy(vt_grid* G) {
   if (!G) return VT_OK;
   cudaSetDevice(G->device);
   if (G->pcg_graph) cudaGraphExecDestroy(G->pcg_graph);
+  if (G->stream) cudaStreamDestroy(G->stream);
   cudaFree(G->mask); cudaFree(G->partial); cudaFree(G->scalars); cudaFreeHost(G->host_scalars);
   cudaFree(G->scratch); cudaFree(G->scratch2);
   double* ws[] = {G->w_x, G->w_f, G->w_r, G->w_p, G->w_q, G->w_z, G->w_t, G->w_d};
@@ -279,6 +293,12 @@ vt_status vt_apply(vt_grid* G, const double* scale, const double* u, double* v, 
   VT_TRY(launch_project(G, u, G->scratch, s));
   return launch_hex8(G, H8_APPLY, false, scale, G->scratch, u, nullptr, v, 0.0, nullptr, nullptr,
                      s);
+}
+
+vt_status vt_apply_projected(vt_grid* G, const double* scale, const double* u, double* v,
+                             void* stream) {
+  return launch_hex8(G, H8_APPLY, false, scale, u, u, nullptr, v, 0.0, nullptr, nullptr,
+                     (cudaStream_t)stream);
 }
 
 vt_status vt_diagonal(vt_grid* G, const double* scale, double* d, void* stream) {
@@ -372,7 +392,11 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
 
 vt_status vt_pcg(vt_grid* G, const double* scale, int precond, vt_hier* H, const double* f,
                  double* x, int warm, double tol, int maxit, vt_solve_report* rep, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+  // The solve is blocking; it runs on a private non-blocking stream so that the
+  // iteration graph can be captured whatever stream (even legacy 0) the caller uses.
+  VT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (!G->stream) VT_CUDA(cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking));
+  cudaStream_t s = G->stream;
   if (!rep) return fail(VT_EINVAL, "null report");
   memset(rep, 0, sizeof(*rep));
   if (precond == 2 && !H) return fail(VT_EINVAL, "multigrid preconditioner needs a hierarchy");

@@ -26,7 +26,9 @@ __global__ void project_kernel(Geom g, const uint8_t* mask, const double* src, d
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
     const long long node = b / 3 + t;
-    const unsigned m = mask[node];
+    const int i = (int)(node % g.rp);
+    const long long r = node / g.rp;
+    const unsigned m = i <= g.nx ? mask[(r / (g.ny + 1)) * g.mplane + (r % (g.ny + 1)) * g.mp + i] : 0u;
 #pragma unroll
     for (int c = 0; c < 3; ++c) dst[node * 3 + c] = ((m >> c) & 1u) ? 0.0 : src[node * 3 + c];
   }
@@ -124,7 +126,7 @@ __global__ void diag_kernel(Geom g, const uint8_t* mask, const double* scale, do
     const int p = (int)(r / (g.ny + 1)) + g.pA;
     const long long node = node_off(g, p, j, i);
     const double d = node_diag(g, scale, p, j, i, kd);
-    const unsigned m = mask[node];
+    const unsigned m = mask[mask_off(g, p, j, i)];
 #pragma unroll
     for (int c = 0; c < 3; ++c) out[node * 3 + c] = ((m >> c) & 1u) ? 1.0 : d;
   }
@@ -151,7 +153,7 @@ __global__ void jacobi0_kernel(Geom g, const uint8_t* mask, const double* scale,
     const int j = (int)(r % (g.ny + 1));
     const int p = (int)(r / (g.ny + 1)) + g.pA;
     const long long node = node_off(g, p, j, i);
-    const unsigned m = mask[node];
+    const unsigned m = mask[mask_off(g, p, j, i)];
     const double d = node_diag(g, scale, p, j, i, kd);
 #pragma unroll
     for (int c = 0; c < 3; ++c)

@@ -55,7 +55,8 @@ struct vt_grid {
   vt::Geom g{};
   double h = 1.0, nu = 0.3;
   vt::Hex8Coef coef{};
-  uint8_t* mask = nullptr;          // node layout (P planes), 1 byte per node
+  uint8_t* mask = nullptr;          // P planes x (ny+1) rows x mp bytes, 1 byte per node
+  CUtensorMap mask_map{};           // TMA descriptor of the mask (48x16 byte boxes)
   long long n_fixed = 0;
   double* partial = nullptr;        // reduction partials (>= 4096 doubles)
   double* scalars = nullptr;        // small device scalar scratch (64 doubles)
@@ -74,6 +75,7 @@ struct vt_grid {
   cudaGraphExec_t pcg_graph = nullptr;
   const void* pcg_key[4] = {nullptr, nullptr, nullptr, nullptr};
   unsigned long long pcg_nodes = 0;   // kernel nodes per PCG iteration graph
+  cudaStream_t stream = nullptr;      // private stream of the blocking solver
 
   long long vec_len() const { return (long long)g.P * g.nplane; }
   long long elem_len() const { return (long long)g.Q * g.eplane; }
