@@ -80,6 +80,10 @@ vt_status vt_grid_destroy(vt_grid *g);
 int64_t vt_vec_len(const vt_grid *g);   /* doubles in a vt node-layout vector  */
 int64_t vt_elem_len(const vt_grid *g);  /* doubles in a vt element-layout field */
 int64_t vt_n_fixed(const vt_grid *g);   /* fixed dofs of this slab              */
+/* Profiling aid: when enabled, every hex8 launch on g records per CTA
+ * {start ns, end ns, smid, items<<32 | tile origin} (4 x uint64); host_out
+ * (optional) receives the last launch's records for max_ctas CTAs. */
+vt_status vt_debug_trace(vt_grid *g, int enable, uint64_t *host_out, int max_ctas);
 
 /* host <-> device conversion between the reference order and vt layout.
  * host pointers may be pageable or pinned; these calls are async on stream. */

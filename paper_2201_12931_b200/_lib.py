@@ -41,6 +41,7 @@ _SIGS = {
     "vt_version": (I, []),
     "vt_launch_count": (C.c_uint64, []),
     "vt_copy": (I, [P, P, I64, P]),
+    "vt_debug_trace": (I, [P, I, P, I]),
     "vt_grid_create": (I, [C.POINTER(P), I, I, I, D, D, P, I, I, I]),
     "vt_grid_destroy": (I, [P]),
     "vt_vec_len": (I64, [P]),

@@ -378,7 +378,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
   auto smooth = [&](int l, bool dot) -> vt_status {
     vt_grid* G = H->lv[l];
     double* dst = (ucur[l] == H->u[l]) ? H->u2[l] : H->u[l];
-    VT_TRY(launch_hex8(G, H8_SMOOTH, dot, H->scale[l], ucur[l], ucur[l], fl[l], dst, H->omega,
+    VT_TRY(launch_hex8(G, H8_SMOOTH, dot, H->scale[l], ucur[l], nullptr, fl[l], dst, H->omega,
                        rz_partial, stop, s));
     ucur[l] = dst;
     return VT_OK;

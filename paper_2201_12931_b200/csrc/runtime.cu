@@ -166,6 +166,24 @@ const char* vt_last_error(void) { return g_err.c_str(); }
 int vt_version(void) { return 1; }
 uint64_t vt_launch_count(void) { return g_launches; }
 
+vt_status vt_debug_trace(vt_grid* G, int enable, uint64_t* host_out, int max_ctas) {
+  if (enable && !G->trace) {
+    VT_CUDA(cudaMalloc(&G->trace, 4 * 8192 * sizeof(unsigned long long)));
+    VT_CUDA(cudaMemset(G->trace, 0, 4 * 8192 * sizeof(unsigned long long)));
+  }
+  if (host_out && G->trace) {
+    VT_CUDA(cudaDeviceSynchronize());
+    const int n = max_ctas < 8192 ? max_ctas : 8192;
+    VT_CUDA(cudaMemcpy(host_out, G->trace, 4 * (size_t)n * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost));
+  }
+  if (!enable && G->trace) {
+    cudaFree(G->trace);
+    G->trace = nullptr;
+  }
+  return VT_OK;
+}
+
 vt_status vt_copy(void* dst, const void* src, int64_t bytes, void* stream) {
   VT_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return VT_OK;
@@ -297,7 +315,7 @@ vt_status vt_apply(vt_grid* G, const double* scale, const double* u, double* v, 
 
 vt_status vt_apply_projected(vt_grid* G, const double* scale, const double* u, double* v,
                              void* stream) {
-  return launch_hex8(G, H8_APPLY, false, scale, u, u, nullptr, v, 0.0, nullptr, nullptr,
+  return launch_hex8(G, H8_APPLY, false, scale, u, nullptr, nullptr, v, 0.0, nullptr, nullptr,
                      (cudaStream_t)stream);
 }
 
@@ -340,7 +358,7 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
   vt_status st = VT_OK;
   do {
     // q = K p, p.q                                    [ref: solver.py:123-124]
-    if ((st = launch_hex8(G, H8_APPLY, true, scale, G->w_p, G->w_p, nullptr, G->w_q, 0.0, P0,
+    if ((st = launch_hex8(G, H8_APPLY, true, scale, G->w_p, nullptr, nullptr, G->w_q, 0.0, P0,
                           &ctl->stop, s)) != VT_OK) break;
     if ((st = launch_pcg_s1(ctl, P0, h8g, s)) != VT_OK) break;
     // x += alpha p ; r -= alpha q | r = f - K x       [ref: solver.py:131-136]

@@ -57,6 +57,7 @@ struct vt_grid {
   vt::Hex8Coef coef{};
   uint8_t* mask = nullptr;          // P planes x (ny+1) rows x mp bytes, 1 byte per node
   CUtensorMap mask_map{};           // TMA descriptor of the mask (48x16 byte boxes)
+  unsigned long long* trace = nullptr;  // per-CTA timing of hex8 launches (vt_debug_trace)
   long long n_fixed = 0;
   double* partial = nullptr;        // reduction partials (>= 4096 doubles)
   double* scalars = nullptr;        // small device scalar scratch (64 doubles)
