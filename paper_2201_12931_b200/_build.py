@@ -34,17 +34,21 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), tag: str = "") -> str:
+    """Compile libvoxb200.so; `defines`/`tag` build a dev variant libvoxb200_<tag>.so
+    (selected at import time with VT_LIB_PATH) for A/B kernel experiments."""
+    obj_dir = OBJ + (f"_{tag}" if tag else "")
+    out = OUT.replace(".so", f"_{tag}.so") if tag else OUT
+    os.makedirs(obj_dir, exist_ok=True)
     nvcc = _nvcc()
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(HERE, "..", "include", "voxb200.h"))
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(obj_dir, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + headers):
-            jobs.append([nvcc, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([nvcc, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", o])
 
     def run(cmd):
         p = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,13 +60,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         logs = list(ex.map(run, jobs))
-    objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
-    if jobs or not os.path.exists(OUT):
-        run([nvcc, *ARCH, "-shared", "-o", OUT, *objs, "-Xcompiler", "-fPIC"])
-    with open(os.path.join(OBJ, "ptxas.log"), "a") as fh:
+    objs = [os.path.join(obj_dir, s.replace(".cu", ".o")) for s in SOURCES]
+    if jobs or not os.path.exists(out):
+        run([nvcc, *ARCH, "-shared", "-o", out, *objs, "-Xcompiler", "-fPIC"])
+    with open(os.path.join(obj_dir, "ptxas.log"), "a") as fh:
         fh.writelines(logs)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    tag = next((a[6:] for a in sys.argv[1:] if a.startswith("--tag=")), "")
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=defs, tag=tag))

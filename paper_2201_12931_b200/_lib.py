@@ -13,7 +13,7 @@ import os
 from .errors import NumericalError, SetupError, SolverBreakdown, VolumeInfeasible
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvoxb200.so")
+LIB_PATH = os.environ.get("VT_LIB_PATH") or os.path.join(_HERE, "libvoxb200.so")
 
 VT_OK, VT_EINVAL, VT_ECUDA, VT_ESETUP, VT_EBREAKDOWN, VT_EVOLUME, VT_ENUMERICAL, VT_ENOMEM, VT_EDENSITY = range(9)
 

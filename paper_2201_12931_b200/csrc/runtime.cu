@@ -119,7 +119,7 @@ const CUtensorMap* vec_map(vt_grid* G, const void* ptr) {
   CUtensorMap m;
   const Geom& g = G->g;
   if (!encode3d(&m, ptr, 3ull * (g.nx + 1), g.ny + 1, g.P, 24ull * g.rp,
-                24ull * g.rp * (g.ny + 1), 100, 17))
+                24ull * g.rp * (g.ny + 1), 100, H8_TY + 1))
     return nullptr;
   if (G->vec_maps.size() > 256) G->vec_maps.clear();
   return &(G->vec_maps[ptr] = m);
@@ -130,7 +130,7 @@ const CUtensorMap* elem_map(vt_grid* G, const void* ptr) {
   if (it != G->elem_maps.end()) return &it->second;
   CUtensorMap m;
   const Geom& g = G->g;
-  if (!encode3d(&m, ptr, g.nx, g.ny, g.Q, 8ull * g.ep, 8ull * g.ep * g.ny, 34, 16)) return nullptr;  // 32 + even-alignment slack
+  if (!encode3d(&m, ptr, g.nx, g.ny, g.Q, 8ull * g.ep, 8ull * g.ep * g.ny, 34, H8_TY)) return nullptr;  // 32 + even-alignment slack
   if (G->elem_maps.size() > 256) G->elem_maps.clear();
   return &(G->elem_maps[ptr] = m);
 }
@@ -244,7 +244,7 @@ vt_status vt_grid_create(vt_grid** out, int nx, int ny, int nz, double h, double
     if (!fn) return fail(VT_ECUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[3] = {(cuuint64_t)nx + 1, (cuuint64_t)ny + 1, (cuuint64_t)g.P};
     cuuint64_t strides[2] = {(cuuint64_t)g.mp, (cuuint64_t)g.mplane};
-    cuuint32_t box[3] = {48, 16, 1}, es[3] = {1, 1, 1};
+    cuuint32_t box[3] = {48, (cuuint32_t)H8_TY, 1}, es[3] = {1, 1, 1};
     if (fn(&G->mask_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, G->mask, dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)

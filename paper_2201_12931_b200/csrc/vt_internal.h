@@ -38,6 +38,12 @@ struct Hex8Coef {
 };
 Hex8Coef hex8_coef(double nu, double h);
 
+// hex8 tile height (element rows per CTA); the TMA boxes of runtime.cu follow it.
+#ifndef VT_H8_TY
+#define VT_H8_TY 16
+#endif
+constexpr int H8_TY = VT_H8_TY;
+
 // Apply-family kernel modes.
 enum Hex8Mode { H8_APPLY = 0, H8_RESID = 1, H8_SMOOTH = 2 };
 
