@@ -194,6 +194,48 @@ vt_status vt_oc_update(vt_grid *g, const double *rho, const int8_t *classes, con
 vt_status vt_change_volume(vt_grid *g, const double *a, const double *b, const int8_t *classes,
                            double *max_abs_diff, double *active_mean, void *stream);
 
+/* ---------------------------------------------------------- z-slab decomposition
+ * The MGPCG solve across ranks (the reference is single-process,
+ * so these entry points have no reference counterpart -- they distribute
+ * vt_apply / vt_hier_* / vt_pcg above).  Rank g owns element layers
+ * [kbounds[g], kbounds[g+1]) of the fine grid; kbounds are multiples of
+ * 2^dist_level, levels 0..dist_level are slab-distributed and the coarse tail
+ * (dist_level+1 .. levels-1, incl. the coarsest direct solve) is replicated.
+ * nccl_id == NULL: all nranks slabs live in this process on `device` and
+ * exchange through device copies (nlocal == nranks); otherwise one slab per
+ * process (nlocal == 1, rank0 = this rank) and NCCL (dlopen'ed, VT_NCCL_LIB)
+ * carries the halos and the rank-ordered dot products.  Slab vectors use the
+ * vt node layout of vt_dist_grid(D, i, 0) (ghost planes included).  Pointer
+ * arrays (`double *const *`) hold one device pointer per local slab. */
+typedef struct vt_dist vt_dist;
+
+int vt_nccl_id_bytes(void);
+vt_status vt_nccl_unique_id(uint8_t *out, int nbytes);
+vt_status vt_dist_create(vt_dist **out, int nx, int ny, int nz, double h, double nu,
+                         const uint8_t *node_mask, int levels, double omega, int nranks,
+                         int rank0, int nlocal, const int *kbounds, int dist_level,
+                         const uint8_t *nccl_id, int device);
+vt_status vt_dist_destroy(vt_dist *D);
+int vt_dist_levels(const vt_dist *D);
+int vt_dist_dist_level(const vt_dist *D);
+int vt_dist_nlocal(const vt_dist *D);
+vt_grid *vt_dist_grid(vt_dist *D, int slab, int level);
+vt_hier *vt_dist_tail(vt_dist *D);
+uint64_t vt_dist_graph_nodes(const vt_dist *D);
+/* level-0 element scales of the local slabs; exchanges the ghost layer */
+vt_status vt_dist_set_scale(vt_dist *D, const double *const *scale0, void *stream);
+/* coarse levels + replicated tail + coarsest factor [ref: multigrid.py:201-233]; blocking */
+vt_status vt_dist_refresh(vt_dist *D, const double *const *rho, const double *const *scale0,
+                          double p, double kmin, double E, void *stream);
+/* v = K u per slab (u zero on fixed dofs; its ghost planes are refreshed) */
+vt_status vt_dist_apply(vt_dist *D, double *const *u, double *const *v, void *stream);
+vt_status vt_dist_dot(vt_dist *D, const double *const *x, const double *const *y, double *out,
+                      void *stream);
+vt_status vt_dist_vcycle(vt_dist *D, const double *const *f, double *const *z, void *stream);
+/* MGPCG over all ranks, same recurrences as vt_pcg [ref: solver.py:62-191]; blocking */
+vt_status vt_dist_pcg(vt_dist *D, const double *const *f, double *const *x, int warm, double tol,
+                      int max_iterations, vt_solve_report *rep, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

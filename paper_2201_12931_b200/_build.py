@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libvoxb200.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["hex8_apply.cu", "vectors.cu", "multigrid.cu", "design.cu", "runtime.cu"]
+SOURCES = ["hex8_apply.cu", "vectors.cu", "multigrid.cu", "design.cu", "runtime.cu", "dist.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]
@@ -62,7 +62,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), tag: str = "")
         logs = list(ex.map(run, jobs))
     objs = [os.path.join(obj_dir, s.replace(".cu", ".o")) for s in SOURCES]
     if jobs or not os.path.exists(out):
-        run([nvcc, *ARCH, "-shared", "-o", out, *objs, "-Xcompiler", "-fPIC"])
+        run([nvcc, *ARCH, "-shared", "-o", out, *objs, "-Xcompiler", "-fPIC", "-ldl"])
     with open(os.path.join(obj_dir, "ptxas.log"), "a") as fh:
         fh.writelines(logs)
     return out

@@ -80,6 +80,22 @@ _SIGS = {
     "vt_filter_correlate": (I, [P, P, P, P]),
     "vt_oc_update": (I, [P, P, P, P, P, D, D, D, D, P, C.POINTER(D), C.POINTER(I), P]),
     "vt_change_volume": (I, [P, P, P, P, C.POINTER(D), C.POINTER(D), P]),
+    "vt_nccl_id_bytes": (I, []),
+    "vt_nccl_unique_id": (I, [P, I]),
+    "vt_dist_create": (I, [C.POINTER(P), I, I, I, D, D, P, I, D, I, I, I, P, I, P, I]),
+    "vt_dist_destroy": (I, [P]),
+    "vt_dist_levels": (I, [P]),
+    "vt_dist_dist_level": (I, [P]),
+    "vt_dist_nlocal": (I, [P]),
+    "vt_dist_grid": (P, [P, I, I]),
+    "vt_dist_tail": (P, [P]),
+    "vt_dist_graph_nodes": (C.c_uint64, [P]),
+    "vt_dist_set_scale": (I, [P, P, P]),
+    "vt_dist_refresh": (I, [P, P, P, D, D, D, P]),
+    "vt_dist_apply": (I, [P, P, P, P]),
+    "vt_dist_dot": (I, [P, P, P, C.POINTER(D), P]),
+    "vt_dist_vcycle": (I, [P, P, P, P]),
+    "vt_dist_pcg": (I, [P, P, P, I, D, I, C.POINTER(SolveReportC), P]),
 }
 
 

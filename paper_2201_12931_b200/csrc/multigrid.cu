@@ -120,15 +120,20 @@ __global__ void count_fixed_kernel(Geom g, const uint8_t* m, unsigned long long*
 // ---------------------------------------------------------------- transfers
 // f_c = P^T r_f, coarse fixed zeroed.  Per axis (z, y, x):
 //   dst[i] = (src[2i] + 0.5 src[2i+1]) + 0.5 src[2i-1]   (missing terms skipped)
+// Coarse node planes [kb, ke) (global); a z-slab of the fine level restricts
+// into the planes whose centre fine plane 2K it owns (its ghost planes hold
+// the neighbours' residual planes 2K0-1 and 2K1-1+1).
 __global__ void restrict_kernel(Geom gf, Geom gc, const uint8_t* mc, const double* __restrict__ rf,
-                                double* __restrict__ fc, const int* stop) {
+                                double* __restrict__ fc, const int* stop, int kb, int ke) {
   if (stop && *(volatile const int*)stop) return;
-  const long long nn = owned_nodes(gc);
+  const long long nn = (long long)(ke - kb) * (gc.ny + 1) * (gc.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
-    int p, J, I;
-    node_coords(gc, t, p, J, I);
-    const int K = p - 1 + gc.k0;
+    const int I = (int)(t % (gc.nx + 1));
+    const long long rr = t / (gc.nx + 1);
+    const int J = (int)(rr % (gc.ny + 1));
+    const int K = (int)(rr / (gc.ny + 1)) + kb;
+    const int p = K - gc.k0 + 1;
     const long long cnode = node_off(gc, p, J, I);
     const unsigned m = mc[mask_off(gc, p, J, I)];
     double out[3];
@@ -179,6 +184,20 @@ __global__ void restrict_kernel(Geom gf, Geom gc, const uint8_t* mc, const doubl
   }
 }
 
+// kb < 0: every coarse plane the coarse grid owns
+vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, const int* stop,
+                          int kb, int ke, cudaStream_t s) {
+  if (kb < 0) {
+    kb = C->g.k0;
+    ke = C->g.k1 + C->g.last;
+  }
+  if (ke <= kb) return VT_OK;
+  restrict_kernel<<<C->nsm * 4, MG_THREADS, 0, s>>>(F->g, C->g, C->mask, rf, fc, stop, kb, ke);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 // u_f (+)= P u_c with fine fixed dofs zeroed in P u_c.  Per axis (z, y, x):
 //   even: dst = src[i/2];  odd: dst = 0.5 * (src[(i-1)/2] + src[(i+1)/2])
 template <bool ADD>
@@ -221,12 +240,35 @@ __global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double
   }
 }
 
+vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
+                             const int* stop, cudaStream_t s) {
+  prolong_kernel<true><<<F->nsm * 8, MG_THREADS, 0, s>>>(C->g, F->g, F->mask, uc, uf, stop);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status launch_coarsen_mask(vt_grid* F, vt_grid* C, cudaStream_t s) {
+  coarsen_mask_kernel<<<C->nsm * 4, MG_THREADS, 0, s>>>(F->g, C->g, F->mask, C->mask);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status launch_coarsen_rho(vt_grid* F, vt_grid* C, const double* rf, double* rc, cudaStream_t s) {
+  coarsen_rho_kernel<<<C->nsm * 4, MG_THREADS, 0, s>>>(F->g.nx, F->g.ny, C->g.nx, C->g.ny,
+                                                      C->g.k1 - C->g.k0, rf, rc);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 // ---------------------------------------------------------------- coarsest level
 // Dense assembly (identity on fixed), in-place Cholesky; one CTA.
 // [ref: multigrid.py:280-316]
 __global__ void __launch_bounds__(1024, 1)
     coarse_factor_kernel(Geom g, const double* scale, const double* k0l, const uint8_t* mask,
-                         int n, double* A, int* status) {
+                         int n, double* A, double* A0, int* status) {
   const int nx1 = g.nx + 1, ny1 = g.ny + 1;
   for (long long t = threadIdx.x; t < (long long)n * n; t += blockDim.x) A[t] = 0.0;
   __syncthreads();
@@ -261,6 +303,7 @@ __global__ void __launch_bounds__(1024, 1)
     }
   }
   __syncthreads();
+  for (long long t = threadIdx.x; t < (long long)n * n; t += blockDim.x) A0[t] = A[t];
   // right-looking Cholesky, lower triangle
   __shared__ double piv;
   __shared__ int bad;
@@ -315,47 +358,71 @@ __global__ void gram_kernel(int n, const double* W, double* Kinv) {
   }
 }
 
-// u = Kinv f on the coarsest level (vt layout in / out, fixed dofs 0)
-__global__ void coarse_solve_kernel(Geom g, const uint8_t* mask, int n, const double* Kinv,
-                                    const double* f, double* u, const int* stop) {
-  if (stop && *(volatile const int*)stop) return;
-  extern __shared__ double fc[];
+// Coarsest solve u = A^{-1} f [ref: multigrid.py:395-402, cho_solve].  The
+// explicit inverse alone (one mat-vec) is not accurate enough: its error is
+// relative to |A^{-1}|, which at SIMP contrasts (kmin = 1e-9) perturbs the
+// preconditioner far more than LAPACK's backward-stable dpotrs does (measured:
+// 3e-5 vs 2e-7 compliance drift over the 40 cfg1 iterations).  One step of
+// iterative refinement with the assembled matrix, x = x0 + Kinv (f - A x0),
+// restores backward stability at the cost of two more dense mat-vecs:
+//   mode 0: fc = gather(f); x0 = Kinv fc          (fc, x0 -> dense scratch)
+//   mode 1: r  = fc - A x0                        (dense scratch)
+//   mode 2: u  = scatter(x0 + Kinv r), fixed -> 0 (vt layout)
+// One warp per row: lane-strided FMAs then the xor tree (fixed order).
+__device__ __forceinline__ void coarse_node(const Geom& g, int d, long long* nd, int* c, int* fixed,
+                                            const uint8_t* mask) {
   const int nx1 = g.nx + 1, ny1 = g.ny + 1;
+  const int node = d / 3;
+  *c = d % 3;
+  const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
+  *nd = node_off(g, k + 1, j, i);
+  if (fixed) *fixed = (mask[mask_off(g, k + 1, j, i)] >> *c) & 1u;
+}
+
+template <int MODE>
+__global__ void coarse_mv_kernel(Geom g, const uint8_t* mask, int n, const double* M,
+                                 const double* f, double* cf, double* x0, double* cr, double* u,
+                                 const int* stop) {
+  if (stop && *(volatile const int*)stop) return;
+  extern __shared__ double vs[];
   for (int d = threadIdx.x; d < n; d += blockDim.x) {
-    const int node = d / 3, c = d % 3;
-    const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
-    fc[d] = f[node_off(g, k + 1, j, i) * 3 + c];
+    double v;
+    if (MODE == 0) {
+      long long nd;
+      int c;
+      coarse_node(g, d, &nd, &c, nullptr, mask);
+      v = f[nd * 3 + c];
+      if (blockIdx.x == 0) cf[d] = v;
+    } else {
+      v = (MODE == 1) ? x0[d] : cr[d];
+    }
+    vs[d] = v;
   }
   __syncthreads();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   for (int r = blockIdx.x * nw + warp; r < n; r += gridDim.x * nw) {
     double s = 0.0;
-    for (int e = lane; e < n; e += 32) s = fma(Kinv[(long long)r * n + e], fc[e], s);
+    for (int e = lane; e < n; e += 32) s = fma(M[(long long)r * n + e], vs[e], s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      const int node = r / 3, c = r % 3;
-      const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
-      const long long nd = node_off(g, k + 1, j, i);
-      u[nd * 3 + c] = ((mask[mask_off(g, k + 1, j, i)] >> c) & 1u) ? 0.0 : s;
+      if (MODE == 0) {
+        x0[r] = s;
+      } else if (MODE == 1) {
+        cr[r] = cf[r] - s;
+      } else {
+        long long nd;
+        int c, fx;
+        coarse_node(g, r, &nd, &c, &fx, mask);
+        u[nd * 3 + c] = fx ? 0.0 : x0[r] + s;
+      }
     }
   }
 }
 
 }  // namespace vt
 
-// ====================================================================== hierarchy
-struct vt_hier {
-  std::vector<vt_grid*> lv;        // lv[0] = caller's fine grid (not owned)
-  std::vector<double*> u, u2, r, f, scale, rho;
-  double omega = 0.4;
-  int sweeps = 1;
-  int nL = 0;                      // coarsest dofs
-  double *A = nullptr, *W = nullptr, *Kinv = nullptr, *k0l = nullptr;
-  int* status = nullptr;
-  bool factored = false;
-  const double* last_z = nullptr;  // buffer that holds the V-cycle output
-};
+// (struct vt_hier lives in vt_internal.h)
 
 namespace vt {
 
@@ -367,14 +434,33 @@ vt_status hier_alloc_vec(vt_grid* G, double** p) {
 
 void hex8_k0_host(double nu, double h, double* K);  // runtime.cu
 
-// Build the level sequence of one V-cycle on `s` (capturable).
+// coarsest solve with one refinement step (3 launches, capturable)
+vt_status launch_coarse_solve(vt_hier* H, const double* f, double* u, const int* stop,
+                              cudaStream_t s) {
+  vt_grid* G = H->lv.back();
+  const int n = H->nL;
+  const size_t sm = (size_t)n * sizeof(double);
+  const int grid = (n + 255) / 256 > 32 ? 32 : (n + 255) / 256;
+  double *cf = H->cvec, *x0 = H->cvec + n, *cr = H->cvec + 2 * n;
+  coarse_mv_kernel<0><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->Kinv, f, cf, x0, cr, u, stop);
+  coarse_mv_kernel<1><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->A0, f, cf, x0, cr, u, stop);
+  coarse_mv_kernel<2><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->Kinv, f, cf, x0, cr, u, stop);
+  count_launch(3);
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// Build the level sequence of one V-cycle on `s` (capturable), entered at
+// level `top` with right-hand side f0 (top > 0: the replicated coarse tail of a
+// z-slab hierarchy, whose level-`top` residual the slabs restricted into
+// H->f[top]; see dist.cu).
 vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, double* rz_partial,
-                             bool want_rz, cudaStream_t s, const double** z_out) {
+                             bool want_rz, cudaStream_t s, const double** z_out, int top) {
   const int L = (int)H->lv.size();
   std::vector<const double*> fl(L);
   std::vector<double*> ucur(L);
-  fl[0] = f0;
   for (int l = 1; l < L; ++l) fl[l] = H->f[l];
+  fl[top] = f0;
   auto smooth = [&](int l, bool dot) -> vt_status {
     vt_grid* G = H->lv[l];
     double* dst = (ucur[l] == H->u[l]) ? H->u2[l] : H->u[l];
@@ -383,7 +469,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
     ucur[l] = dst;
     return VT_OK;
   };
-  for (int l = 0; l < L - 1; ++l) {
+  for (int l = top; l < L - 1; ++l) {
     vt_grid* G = H->lv[l];
     ucur[l] = H->u[l];
     if (H->sweeps >= 1) {
@@ -391,26 +477,19 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
       for (int k = 1; k < H->sweeps; ++k) VT_TRY(smooth(l, false));
       VT_TRY(launch_hex8(G, H8_RESID, false, H->scale[l], ucur[l], ucur[l], fl[l], H->r[l], 0.0,
                          nullptr, stop, s));
-      restrict_kernel<<<H->lv[l + 1]->nsm * 4, MG_THREADS, 0, s>>>(
-          G->g, H->lv[l + 1]->g, H->lv[l + 1]->mask, H->r[l], H->f[l + 1], stop);
+      VT_TRY(launch_restrict(G, H->lv[l + 1], H->r[l], H->f[l + 1], stop, -1, -1, s));
     } else {
       VT_TRY(launch_zero_owned(G, H->u[l], s));
-      restrict_kernel<<<H->lv[l + 1]->nsm * 4, MG_THREADS, 0, s>>>(
-          G->g, H->lv[l + 1]->g, H->lv[l + 1]->mask, fl[l], H->f[l + 1], stop);
+      VT_TRY(launch_restrict(G, H->lv[l + 1], fl[l], H->f[l + 1], stop, -1, -1, s));
     }
-    count_launch();
-    VT_CUDA(cudaGetLastError());
   }
   {
     vt_grid* G = H->lv[L - 1];
-    const size_t sm = (size_t)H->nL * sizeof(double);
-    coarse_solve_kernel<<<(H->nL + 255) / 256 > 32 ? 32 : (H->nL + 255) / 256, 256, sm, s>>>(
-        G->g, G->mask, H->nL, H->Kinv, fl[L - 1], H->u[L - 1], stop);
-    count_launch();
-    VT_CUDA(cudaGetLastError());
+    (void)G;
+    VT_TRY(launch_coarse_solve(H, fl[L - 1], H->u[L - 1], stop, s));
     ucur[L - 1] = H->u[L - 1];
   }
-  for (int l = L - 2; l >= 0; --l) {
+  for (int l = L - 2; l >= top; --l) {
     vt_grid* G = H->lv[l];
     prolong_kernel<true><<<G->nsm * 8, MG_THREADS, 0, s>>>(H->lv[l + 1]->g, G->g, G->mask,
                                                            ucur[l + 1], ucur[l], stop);
@@ -418,8 +497,8 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
     VT_CUDA(cudaGetLastError());
     for (int k = 0; k < H->sweeps; ++k) VT_TRY(smooth(l, want_rz && l == 0 && k == H->sweeps - 1));
   }
-  *z_out = ucur[0];
-  H->last_z = ucur[0];
+  *z_out = ucur[top];
+  if (top == 0) H->last_z = ucur[0];
   return VT_OK;
 }
 
@@ -496,7 +575,7 @@ vt_status vt_hier_destroy(vt_hier* H) {
     cudaFree(H->scale[l]); cudaFree(H->rho[l]);
     if (l > 0) vt_grid_destroy(H->lv[l]);
   }
-  cudaFree(H->A); cudaFree(H->W); cudaFree(H->Kinv); cudaFree(H->k0l); cudaFree(H->status);
+  cudaFree(H->A); cudaFree(H->A0); cudaFree(H->cvec); cudaFree(H->W); cudaFree(H->Kinv); cudaFree(H->k0l); cudaFree(H->status);
   delete H;
   return VT_OK;
 }
@@ -541,17 +620,25 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
     VT_CUDA(cudaMalloc(&H->A, (size_t)n * n * sizeof(double)));
     VT_CUDA(cudaMalloc(&H->W, (size_t)n * n * sizeof(double)));
     VT_CUDA(cudaMalloc(&H->Kinv, (size_t)n * n * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->A0, (size_t)n * n * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->cvec, 3 * (size_t)n * sizeof(double)));
     VT_CUDA(cudaMalloc(&H->k0l, 576 * sizeof(double)));
     VT_CUDA(cudaMalloc(&H->status, sizeof(int)));
     double K[576];
     hex8_k0_host(C->nu, C->h, K);
     VT_CUDA(cudaMemcpy(H->k0l, K, sizeof(K), cudaMemcpyHostToDevice));
     if ((size_t)n * sizeof(double) > 48 * 1024)
-      VT_CUDA(cudaFuncSetAttribute(coarse_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+      VT_CUDA(cudaFuncSetAttribute(coarse_mv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(n * sizeof(double))));
+      VT_CUDA(cudaFuncSetAttribute(coarse_mv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(n * sizeof(double))));
+      VT_CUDA(cudaFuncSetAttribute(coarse_mv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(n * sizeof(double))));
+    }
   }
   coarse_factor_kernel<<<1, 1024, 0, s>>>(C->g, H->scale[L - 1], H->k0l, C->mask, n, H->A,
-                                          H->status);
+                                          H->A0, H->status);
   tri_inverse_kernel<<<(n + 127) / 128, 128, 0, s>>>(n, H->A, H->W);
   gram_kernel<<<C->nsm * 4, 256, 0, s>>>(n, H->W, H->Kinv);
   count_launch(3);
@@ -586,11 +673,7 @@ vt_status vt_hier_restrict(vt_hier* H, int l, const double* fine, double* coarse
   if (l < 0 || l + 1 >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
   vt_grid* F = H->lv[l];
   VT_TRY(launch_project(F, fine, F->scratch, s));
-  restrict_kernel<<<H->lv[l + 1]->nsm * 4, MG_THREADS, 0, s>>>(F->g, H->lv[l + 1]->g,
-                                                               H->lv[l + 1]->mask, F->scratch,
-                                                               coarse, nullptr);
-  count_launch();
-  VT_CUDA(cudaGetLastError());
+  VT_TRY(launch_restrict(F, H->lv[l + 1], F->scratch, coarse, nullptr, -1, -1, s));
   return VT_OK;
 }
 
@@ -635,13 +718,7 @@ vt_status vt_hier_level_diag(vt_hier* H, int l, double* d, void* stream) {
 vt_status vt_hier_coarse_solve(vt_hier* H, const double* f, double* u, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (!H->factored) return fail(VT_ESETUP, "hierarchy was not refreshed before use");
-  vt_grid* G = H->lv.back();
-  const size_t sm = (size_t)H->nL * sizeof(double);
-  coarse_solve_kernel<<<(H->nL + 255) / 256 > 32 ? 32 : (H->nL + 255) / 256, 256, sm, s>>>(
-      G->g, G->mask, H->nL, H->Kinv, f, u, nullptr);
-  count_launch();
-  VT_CUDA(cudaGetLastError());
-  return VT_OK;
+  return launch_coarse_solve(H, f, u, nullptr, s);
 }
 
 }  // extern "C"

@@ -137,9 +137,7 @@ const CUtensorMap* elem_map(vt_grid* G, const void* ptr) {
 
 vt_status launch_scale(vt_grid* G, const double* rho, double p, double kmin, double E,
                        double* scale, int* bad, cudaStream_t s);
-vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, double* rz_partial,
-                             bool want_rz, cudaStream_t s, const double** z_out);
-int hier_rz_parts(vt_hier* H);
+
 
 static vt_status alloc_vec(vt_grid* G, double** p) {
   if (*p) return VT_OK;

@@ -176,8 +176,11 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
                                   const double* __restrict__ p, double* __restrict__ r,
                                   const double* __restrict__ q, double* partial, int with_r) {
   __shared__ double red[VT_THREADS / 32];
+  // The host enqueues iteration k+1 before it sees that iteration k stopped, so
+  // every pass of an iteration checks `stop` itself: S1 of a stopped solve
+  // returns early and leaves the skip flags of the last live iteration behind.
   const int skip = with_r ? ctl->skip_rec : ctl->skip_true50;
-  if (skip) return;
+  if (skip || ctl->stop) return;
   const double alpha = ctl->alpha;
   long long b, e;
   owned_range(g, b, e);
@@ -212,7 +215,7 @@ __global__ void pcg_xpby_kernel(Geom g, const PcgCtl* ctl, const double* __restr
 // conditional copy dst = src (skip flag)
 __global__ void copy_kernel(Geom g, const int* skip, const double* __restrict__ src,
                             double* __restrict__ dst) {
-  if (skip && *(volatile const int*)skip) return;
+  if (skip && *(volatile const int*)skip) return;  // (skip_swap is 1 once stopped)
   long long b, e;
   owned_range(g, b, e);
   for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
@@ -290,6 +293,7 @@ __global__ void pcg_s3_kernel(PcgCtl* c, const double* partial, int n) {
   if (trel <= c->tol) {
     c->converged = 1;
     c->stop = 1;
+    c->skip_rec = c->skip_true50 = c->skip_cand = c->skip_swap = 1;
   } else {
     c->skip_swap = 0;
   }

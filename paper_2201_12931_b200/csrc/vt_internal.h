@@ -40,7 +40,7 @@ Hex8Coef hex8_coef(double nu, double h);
 
 // hex8 tile height (element rows per CTA); the TMA boxes of runtime.cu follow it.
 #ifndef VT_H8_TY
-#define VT_H8_TY 16
+#define VT_H8_TY 8
 #endif
 constexpr int H8_TY = VT_H8_TY;
 
@@ -89,6 +89,21 @@ struct vt_grid {
   long long nel_local() const { return (long long)g.nx * g.ny * (g.k1 - g.k0); }
 };
 
+// ------------------------------------------------------------------- hierarchy
+struct vt_hier {
+  std::vector<vt_grid*> lv;        // lv[0] = caller's fine grid (not owned)
+  std::vector<double*> u, u2, r, f, scale, rho;
+  double omega = 0.4;
+  int sweeps = 1;
+  int nL = 0;                      // coarsest dofs
+  double *A = nullptr, *W = nullptr, *Kinv = nullptr, *k0l = nullptr;
+  double* A0 = nullptr;             // assembled coarsest matrix (refinement residual)
+  double* cvec = nullptr;           // 3 dense coarsest vectors: fc, x0, r
+  int* status = nullptr;
+  bool factored = false;
+  const double* last_z = nullptr;  // buffer that holds the V-cycle output
+};
+
 namespace vt {
 // TMA descriptors (cached per device pointer)
 const CUtensorMap* vec_map(vt_grid* G, const void* ptr);
@@ -108,4 +123,16 @@ vt_status launch_sum_partials(const double* partial, int n, double* out, cudaStr
 vt_status launch_diag(vt_grid* G, const double* scale, double* d, cudaStream_t s);
 vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s);
 int dot_grid(vt_grid* G);
+// (multigrid.cu)
+vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, double* rz_partial,
+                             bool want_rz, cudaStream_t s, const double** z_out, int top = 0);
+int hier_rz_parts(vt_hier* H);
+vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
+                             const int* stop, cudaStream_t s);
+vt_status launch_coarsen_mask(vt_grid* F, vt_grid* C, cudaStream_t s);
+vt_status launch_coarsen_rho(vt_grid* F, vt_grid* C, const double* rf, double* rc, cudaStream_t s);
+vt_status launch_scale(vt_grid* G, const double* rho, double p, double kmin, double E,
+                       double* scale, int* bad, cudaStream_t s);
+vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, const int* stop,
+                          int kb, int ke, cudaStream_t s);
 }  // namespace vt

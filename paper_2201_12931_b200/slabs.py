@@ -1,0 +1,240 @@
+"""Z-slab decomposition of the MGPCG solve: one slab per rank.
+
+The reference is single-process; this module distributes its state-equation
+solve -- the matrix-free K(rho)u, the homogenized V-cycle and PCG -- over
+z-slabs (csrc/dist.cu).  Levels 0..D are slab-distributed with one ghost node
+plane per side (NCCL send/recv halos); the coarse tail D+1..L-1, including the
+dense coarsest solve, is replicated on every rank; dot products are reduced
+per rank, all-gathered and summed in rank order so every rank takes the same
+scalar decisions.
+
+Two transports, same arithmetic:
+  * ``SlabSolver(..., nranks=N)`` without a process group keeps all N slabs in
+    this process on one GPU (halos are device copies) -- used by the parity
+    tests, which compare it with the single-slab solve;
+  * ``SlabSolver.from_process_group(...)`` runs one slab per rank of an
+    initialised ``torch.distributed`` group (torchrun, one process per GPU);
+    the library creates its own NCCL communicator from an id broadcast over
+    that group.
+
+``plan_slabs`` (pure host logic, gloo-tested on CPU) chooses the partition.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from ._lib import SolveReportC, check, lib
+from .device import DeviceGrid, ptr, require_cuda, stream_ptr
+from .hierarchy import max_feasible_levels
+from .krylov import SolveReport, SolverConfig
+from .material import MaterialModel
+from .mesh import StructuredGrid, node_mask_bytes
+
+__all__ = ["SlabPlan", "plan_slabs", "SlabSolver"]
+
+
+@dataclass(frozen=True)
+class SlabPlan:
+    """Partition of the element layers: rank g owns [bounds[g], bounds[g+1])."""
+
+    nranks: int
+    levels: int
+    dist_level: int          # levels 0..dist_level are slab-distributed
+    bounds: Tuple[int, ...]  # nranks + 1 layer boundaries, multiples of 2**dist_level
+
+    def slab(self, rank: int) -> Tuple[int, int]:
+        return self.bounds[rank], self.bounds[rank + 1]
+
+    def tail_planes(self, rank: int, nz: int) -> Tuple[int, int]:
+        """Coarse node planes of level dist_level+1 restricted by `rank` (those
+        whose centre fine plane 2K the rank owns at level dist_level)."""
+        d = self.dist_level
+        a = self.bounds[rank] >> d
+        b = (self.bounds[rank + 1] >> d) + (1 if self.bounds[rank + 1] == nz else 0)
+        return (a + 1) // 2, (b + 1) // 2
+
+    def halo_pattern(self, rank: int) -> List[Tuple[str, int, int]]:
+        """Per-apply node-plane exchange of `rank` as (op, peer, local plane p):
+        send the first owned plane down / the last owned plane up, receive the
+        ghost planes p = 0 and p = n + 1 (mirrors csrc/dist.cu halo_nodes)."""
+        k0, k1 = self.slab(rank)
+        n = k1 - k0
+        ops = []
+        if rank > 0:
+            ops += [("send", rank - 1, 1), ("recv", rank - 1, 0)]
+        if rank < self.nranks - 1:
+            ops += [("send", rank + 1, n), ("recv", rank + 1, n + 1)]
+        return ops
+
+
+def plan_slabs(nz: int, levels: int, nranks: int) -> SlabPlan:
+    """Even z-slabs whose boundaries survive the deepest possible coarsening.
+
+    D = the largest level d <= levels-2 at which nz / 2**d layers split evenly
+    into nranks slabs (so every distributed level is balanced and every slab
+    boundary falls on an even coarse layer); levels d+1.. are replicated."""
+    if nranks < 1:
+        raise ValueError("nranks must be positive")
+    if levels < 2:
+        raise ValueError("the slab solver needs at least 2 multigrid levels")
+    if nz % (1 << (levels - 1)):
+        raise ValueError(f"nz={nz} does not support {levels} levels")
+    for d in range(levels - 2, -1, -1):
+        t = nz >> d
+        if t % nranks == 0:
+            per = (t // nranks) << d
+            return SlabPlan(nranks, levels, d, tuple(per * g for g in range(nranks + 1)))
+    raise ValueError(f"cannot split nz={nz} element layers evenly into {nranks} slabs")
+
+
+def _ptr_array(tensors: Sequence[torch.Tensor]):
+    arr = (C.c_void_p * len(tensors))()
+    for i, t in enumerate(tensors):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+class SlabSolver:
+    """Slab-decomposed operator + homogenized MGPCG for one problem.
+
+    grid / fixed_mask are the global problem (every rank passes the same).
+    Vectors are lists of per-local-slab device tensors in the vt node layout
+    of the slab grid (``upload`` / ``download`` convert global numpy arrays)."""
+
+    def __init__(self, grid: StructuredGrid, fixed_mask, levels: Optional[int] = None, omega: float = 0.4,
+                 nranks: int = 1, rank: int = 0, nlocal: Optional[int] = None, nccl_id: Optional[bytes] = None,
+                 nu: float = 0.3, device: Optional[int] = None):
+        require_cuda()
+        self.grid = grid
+        self.levels = int(levels) if levels is not None else max_feasible_levels(grid.nelx, grid.nely, grid.nelz)
+        self.plan = plan_slabs(grid.nelz, self.levels, nranks)
+        self.nranks, self.rank = nranks, rank
+        self.nlocal = nranks if nlocal is None else int(nlocal)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        mask = np.asarray(fixed_mask, dtype=bool)
+        if mask.shape != (grid.n_dofs,):
+            raise ValueError("fixed mask has wrong length")
+        self.fixed_mask = mask
+        nm = node_mask_bytes(mask)
+        kb = (C.c_int * (nranks + 1))(*self.plan.bounds)
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (C.c_uint8 * len(nccl_id)).from_buffer_copy(nccl_id)
+        self._h = C.c_void_p()
+        check(lib.vt_dist_create(C.byref(self._h), grid.nelx, grid.nely, grid.nelz, grid.h, nu,
+                                 nm.ctypes.data_as(C.c_void_p), self.levels, omega, nranks, rank,
+                                 self.nlocal, kb, self.plan.dist_level, idbuf, self.device), "vt_dist_create")
+        self.slab_grids = []
+        for i in range(self.nlocal):
+            g = lib.vt_dist_grid(self._h, i, 0)
+            k0, k1 = self.plan.slab(rank + i)
+            dg = DeviceGrid.wrap(g, grid.nelx, grid.nely, grid.nelz, grid.h, nu, self.device)
+            dg.k0, dg.k1 = k0, k1
+            dg.vec_len = int(lib.vt_vec_len(C.c_void_p(g)))
+            dg.elem_len = int(lib.vt_elem_len(C.c_void_p(g)))
+            self.slab_grids.append(dg)
+        self.scales = [dg.zeros_elem() for dg in self.slab_grids]
+        self.model: Optional[MaterialModel] = None
+
+    @classmethod
+    def from_process_group(cls, grid: StructuredGrid, fixed_mask, levels=None, omega=0.4, group=None):
+        """One slab per rank of the initialised torch.distributed group; the
+        library's NCCL communicator is bootstrapped from an id broadcast over it."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        nbytes = int(lib.vt_nccl_id_bytes())
+        obj = [None]
+        if rank == 0:
+            buf = (C.c_uint8 * nbytes)()
+            check(lib.vt_nccl_unique_id(buf, nbytes), "vt_nccl_unique_id")
+            obj[0] = bytes(buf)
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nccl_id=obj[0])
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.vt_dist_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ data movement
+    def upload(self, host) -> List[torch.Tensor]:
+        return [dg.upload(host) for dg in self.slab_grids]
+
+    def download(self, vecs: Sequence[torch.Tensor], out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Owned planes of the local slabs into a global (n_dofs,) array."""
+        out = np.zeros(self.grid.n_dofs) if out is None else out
+        for dg, v in zip(self.slab_grids, vecs):
+            check(lib.vt_vec_download(dg.handle, ptr(v), out.ctypes.data_as(C.c_void_p), stream_ptr()))
+        torch.cuda.current_stream().synchronize()
+        return out
+
+    def zeros(self) -> List[torch.Tensor]:
+        return [dg.zeros() for dg in self.slab_grids]
+
+    def _slab_rho(self, rho) -> List[torch.Tensor]:
+        nxy = self.grid.nelx * self.grid.nely
+        rho_t = rho if isinstance(rho, torch.Tensor) else torch.as_tensor(np.asarray(rho, dtype=np.float64))
+        rho_t = rho_t.to(device=f"cuda:{self.device}", dtype=torch.float64)
+        if rho_t.shape != (self.grid.n_elements,):
+            raise ValueError(f"densities must have length {self.grid.n_elements}")
+        return [rho_t[dg.k0 * nxy:dg.k1 * nxy].contiguous() for dg in self.slab_grids]
+
+    # ------------------------------------------------------------ operator / MG
+    def set_density(self, rho, model: MaterialModel = MaterialModel(), refresh: bool = True):
+        """scale = E s(rho) per slab (+ ghost layer); refresh = coarse levels + coarsest factor."""
+        self.model = model
+        self._rho = self._slab_rho(rho)
+        for dg, r, sc in zip(self.slab_grids, self._rho, self.scales):
+            check(lib.vt_scale_from_density(dg.handle, ptr(r), model.p, model.kmin_frac, model.E, ptr(sc),
+                                            stream_ptr()))
+        if refresh:
+            check(lib.vt_dist_refresh(self._h, _ptr_array(self._rho), _ptr_array(self.scales), model.p,
+                                      model.kmin_frac, model.E, stream_ptr()), "vt_dist_refresh")
+        else:
+            check(lib.vt_dist_set_scale(self._h, _ptr_array(self.scales), stream_ptr()))
+
+    def apply(self, u: List[torch.Tensor], v: Optional[List[torch.Tensor]] = None) -> List[torch.Tensor]:
+        """v = K u on every local slab (u zero on fixed dofs; its ghost planes are refreshed)."""
+        v = self.zeros() if v is None else v
+        check(lib.vt_dist_apply(self._h, _ptr_array(u), _ptr_array(v), stream_ptr()))
+        return v
+
+    def dot(self, x: List[torch.Tensor], y: List[torch.Tensor]) -> float:
+        out = C.c_double()
+        check(lib.vt_dist_dot(self._h, _ptr_array(x), _ptr_array(y), C.byref(out), stream_ptr()))
+        return out.value
+
+    def v_cycle(self, f: List[torch.Tensor]) -> List[torch.Tensor]:
+        z = self.zeros()
+        check(lib.vt_dist_vcycle(self._h, _ptr_array(f), _ptr_array(z), stream_ptr()), "vt_dist_vcycle")
+        return z
+
+    def mgcg_solve(self, f: List[torch.Tensor], u_prev: Optional[List[torch.Tensor]] = None,
+                   cfg: SolverConfig = SolverConfig()) -> Tuple[List[torch.Tensor], SolveReport]:
+        """MGPCG over all ranks (solver.py:170-191 with the pcg of 62-167)."""
+        if cfg.preconditioner != "multigrid":
+            raise ValueError("the slab solver implements the multigrid preconditioner")
+        x = [t.clone() for t in u_prev] if (u_prev is not None and cfg.warm_start) else self.zeros()
+        rep = SolveReportC()
+        t0 = time.perf_counter()
+        check(lib.vt_dist_pcg(self._h, _ptr_array(f), _ptr_array(x), 1 if u_prev is not None and cfg.warm_start else 0,
+                              float(cfg.tolerance), int(cfg.max_iterations), C.byref(rep), stream_ptr()),
+              "vt_dist_pcg")
+        return x, SolveReport(iterations=rep.iterations, final_rel_residual=rep.final_rel_residual,
+                              precond_applications=rep.precond_applications, wall_s=time.perf_counter() - t0,
+                              converged=bool(rep.converged), aux_vector_scalars=0,
+                              residual_drift=rep.residual_drift)
