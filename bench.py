@@ -13,8 +13,10 @@ reported beside it ("solve"), from real SIMP iterations of the design loop.
 `e2e` is the same metric through the public Python API with host numpy
 buffers (H2D + kernel + D2H inside the timed region).
 
-Under torchrun (N > 1) every rank runs its own cfg2 replica (weak scaling);
-the z-slab decomposition with NCCL halos is the next step.
+Under torchrun (N > 1) the same global problem is split into N z-slabs, one
+per GPU (paper_2201_12931_b200.slabs, csrc/dist.cu): every step exchanges one
+node plane with each neighbour over NCCL, then applies the operator to the
+slab (strong scaling; value = global dofs / max-over-ranks step time).
 --impl reference times the reference algorithm's CPU implementation (the
 numpy oracle restatement, oracle/cpu_path.py) on this host's cores.
 """
@@ -102,6 +104,20 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- ours
+def _timed(fn, steps, stream):
+    """CUDA-event time per call of `fn` on `stream` (synchronised both sides)."""
+    import torch
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / steps
+
+
 def run_ours(a):
     import numpy as np
     import torch
@@ -140,62 +156,91 @@ def run_ours(a):
     rng = np.random.default_rng(0)
     rho = rng.uniform(0.0, 1.0, nel)
     fm = problem.boundary.fixed_mask(grid)
-    state = vb.OperatorState(grid, rho, problem.model, fm, problem.stiffness())
-    d = state.dgrid
     u_host = rng.standard_normal(n)
     u_host[fm] = 0.0
-    u = d.upload(u_host)
-    v = d.zeros()
     stream = torch.cuda.current_stream()
     sp = stream_ptr()
+    pin_u = torch.from_numpy(u_host).pin_memory()
+    u_np = pin_u.numpy()
+    hbm_peak, peak_src = _peaks()
+    solve = None
 
-    def step():
-        lib.vt_apply_projected(d.handle, ptr(state.scale_dev), ptr(u), ptr(v), sp)
+    if world == 1:
+        # ---- value: device-resident K(rho)u (the operator CG applies every iteration)
+        state = vb.OperatorState(grid, rho, problem.model, fm, problem.stiffness())
+        d = state.dgrid
+        u = d.upload(u_host)
+        v = d.zeros()
+
+        def step():
+            lib.vt_apply_projected(d.handle, ptr(state.scale_dev), ptr(u), ptr(v), sp)
+
+        # ---- e2e: the public apply(), numpy (pinned) in -> numpy out; H2D + D2H per call
+        def e2e_step():
+            return vb.apply(state, u_np)
+
+        parallelism = "1 GPU"
+        scaling = "weak"
+    else:
+        # ---- z-slab decomposition of the same global problem (strong scaling):
+        # one slab per rank, NCCL halo planes before every apply
+        from paper_2201_12931_b200.slabs import SlabSolver
+
+        S = SlabSolver.from_process_group(grid, fm, levels=spec["levels"])
+        S.set_density(rho, problem.model)
+        us = S.upload(u_host)
+        vs = S.zeros()
+        uarr = [t.data_ptr() for t in us]
+        import ctypes as C
+
+        up = (C.c_void_p * 1)(uarr[0])
+        vp = (C.c_void_p * 1)(vs[0].data_ptr())
+
+        def step():
+            lib.vt_dist_apply(S._h, up, vp, sp)
+
+        def e2e_step():
+            return S.download(S.apply(S.upload(u_np)))
+
+        parallelism = f"{world} z-slabs (NCCL halo planes), layers {list(S.plan.bounds)}"
+        scaling = "strong"
 
     for _ in range(max(a.warmup, 3)):
         step()
     barrier()
     l0 = vb.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
-        e0.record(stream)
-        for _ in range(a.steps):
-            step()
-        e1.record(stream)
-        e1.synchronize()
+        t_step = _timed(step, a.steps, stream)
         barrier()
     launches = vb.launch_count() - l0
-    t_step = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / a.steps)
-    gdofs = world * n / t_step / 1e9
-    alg_bytes = 16.0 * n + 8.0 * nel  # read u, write v (8 B/dof each) + read scale (8 B/element)
-    hbm_peak, peak_src = _peaks()
+    t_step = max_over_ranks(t_step)
+    gdofs = n / t_step / 1e9  # whole-job: the global problem's dofs per step
+    # algorithmic bytes: read u, write v (8 B/dof each) + read scale (8 B/element); per rank
+    alg_bytes = (16.0 * n + 8.0 * nel) / world
     achieved = alg_bytes / t_step / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
-    if os.path.exists(tf):
+    if world == 1 and os.path.exists(tf):
         try:
             traffic = json.load(open(tf)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
-    # ---- e2e: public API, host numpy in -> numpy out (pinned host buffers)
-    pin_u = torch.from_numpy(u_host).pin_memory()
-    u_np = pin_u.numpy()
-    for _ in range(2):
-        vb.apply(state, u_np)
-    torch.cuda.synchronize()
+    out = None
+    for _ in range(3):  # steady state: the caching pinned allocator holds the alternating outputs
+        out = e2e_step()
+    barrier()
     ke = max(3, a.steps // 4)
     t0 = time.perf_counter()
     for _ in range(ke):
-        out = vb.apply(state, u_np)
+        out = e2e_step()
     torch.cuda.synchronize()
     t_e2e = max_over_ranks((time.perf_counter() - t0) / ke)
     assert out.shape == (n,)
 
-    # ---- MGPCG solve per SIMP iteration (real design iterations of the same problem)
-    solve = None
-    if a.simp_iters > 0:
+    # ---- MGPCG solve per SIMP iteration
+    if a.simp_iters > 0 and world == 1:
         opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
         R = DeviceRun(problem, opt, vb.SolverConfig(tolerance=1e-5), "homogenized", spec["levels"], 0.4)
         times, its = [], []
@@ -208,11 +253,25 @@ def run_ours(a):
             times.append(time.perf_counter() - ts)
             its.append(rep.iterations)
             R.design_step(model)
-        barrier()
-        ts_mean = max_over_ranks(sum(times) / len(times))
-        solve = {"s_per_simp_iter": ts_mean, "simp_iters": a.simp_iters, "cg_iters": its,
+        solve = {"s_per_simp_iter": sum(times) / len(times), "simp_iters": a.simp_iters, "cg_iters": its,
                  "ms_per_cg_iter": 1e3 * sum(times) / max(1, sum(its)), "levels": R.hier.n_levels,
-                 "note": "first SIMP iterations of the cfg design loop (homogenized MG, V(1,1), tol 1e-5)"}
+                 "note": "first SIMP iterations of the cfg design loop (refresh + homogenized MGPCG, "
+                         "V(1,1), tol 1e-5, warm start)"}
+    elif a.simp_iters > 0:
+        f = problem.boundary.external_force(grid)
+        f[fm] = 0.0
+        rho0 = np.full(nel, spec["volfrac"])
+        barrier()
+        ts = time.perf_counter()
+        S.set_density(rho0, problem.model)
+        x, rep = S.mgcg_solve(S.upload(f), cfg=vb.SolverConfig(tolerance=1e-5))
+        barrier()
+        t_solve = max_over_ranks(time.perf_counter() - ts)
+        solve = {"s_per_simp_iter": t_solve, "simp_iters": 1, "cg_iters": [rep.iterations],
+                 "ms_per_cg_iter": 1e3 * t_solve / max(1, rep.iterations), "levels": S.levels,
+                 "dist_level": S.plan.dist_level,
+                 "note": "SIMP iteration 1 system (uniform volfrac densities): refresh + slab MGPCG, "
+                         "tol 1e-5, max over ranks"}
 
     res = {
         "metric": METRIC,
@@ -223,19 +282,23 @@ def run_ours(a):
         "warmup": a.warmup,
         "ms_per_step": t_step * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (rho ~ U(0,1), u ~ N(0,1), seed 0)",
-        "config": {"workload": f"{a.config} cantilever {nx}x{ny}x{nz} hex8 matrix-free K(rho)u, "
-                               f"{n} dofs, {nel} elements", "dofs": n, "elements": nel,
-                   "parallelism": f"{world} independent replicas" if world > 1 else "1 GPU",
-                   "l2": "inputs larger than L2 (apply working set %.0f MB > 126 MB)" % (alg_bytes / 1e6)},
+        "config": {"workload": f"{a.config} {spec['builder'].__name__} {nx}x{ny}x{nz} hex8 matrix-free "
+                               f"K(rho)u, {n} dofs, {nel} elements", "dofs": n, "elements": nel,
+                   "parallelism": parallelism,
+                   "l2": "inputs larger than L2 (apply working set %.0f MB per GPU > 126 MB)" % (alg_bytes / 1e6)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg_bytes},
-        "e2e": {"value": world * n / t_e2e / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n,
-                "d2h_bytes_per_step": 8 * n},
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel": "hex8_tile_kernel<APPLY> (+ NCCL halo planes when N > 1)"},
+        "e2e": {"value": n / t_e2e / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n,
+                "path": "paper_2201_12931_b200.apply(state, pinned numpy) -> numpy (vt_apply_host, "
+                        "z-chunked H2D/kernel/D2H overlap)" if world == 1 else
+                        "SlabSolver.upload -> apply -> download (host numpy, per-rank planes)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "solve": solve,
@@ -243,6 +306,7 @@ def run_ours(a):
     if rank == 0 and world == 1 and not a.no_cpu:
         res["cpu_baseline"] = cpu_baseline(a.config, reps=2)
     if world > 1:
+        S.close()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(res))

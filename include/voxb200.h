@@ -105,6 +105,12 @@ vt_status vt_apply(vt_grid *g, const double *scale, const double *u, double *v, 
  * multigrid vector is); skips the projection pass of vt_apply. */
 vt_status vt_apply_projected(vt_grid *g, const double *scale, const double *u, double *v,
                              void *stream);
+/* v = K(rho) u from HOST memory to HOST memory (reference (n_dofs,) order),
+ * streamed in `nchunks` z-chunks so the H2D copy, the operator and the D2H
+ * copy overlap [ref: operator.py:154-165]; fixed dofs keep u (identity).
+ * Pinned host buffers give full PCIe bandwidth.  Blocking. */
+vt_status vt_apply_host(vt_grid *g, const double *scale, const double *u_host, double *v_host,
+                        int nchunks, void *stream);
 /* d = diag K, 1 on fixed [ref: operator.py:84-105, 168-174] */
 vt_status vt_diagonal(vt_grid *g, const double *scale, double *d, void *stream);
 /* r = f - K u, zero on fixed [ref: operator.py:177-184] */

@@ -52,6 +52,7 @@ _SIGS = {
     "vt_scale_from_density": (I, [P, P, D, D, D, P, P]),
     "vt_apply": (I, [P, P, P, P, P]),
     "vt_apply_projected": (I, [P, P, P, P, P]),
+    "vt_apply_host": (I, [P, P, P, P, I, P]),
     "vt_diagonal": (I, [P, P, P, P]),
     "vt_residual": (I, [P, P, P, P, P, P]),
     "vt_dot": (I, [P, P, P, C.POINTER(D), P]),

@@ -259,6 +259,11 @@ vt_status vt_grid_destroy(vt_grid* G) {
   if (G->stream) cudaStreamDestroy(G->stream);
   cudaFree(G->mask); cudaFree(G->partial); cudaFree(G->scalars); cudaFreeHost(G->host_scalars);
   cudaFree(G->scratch); cudaFree(G->scratch2);
+  cudaFree(G->io_stage); cudaFree(G->io_raw); cudaFree(G->io_proj); cudaFree(G->io_v);
+  if (G->io_in) cudaStreamDestroy(G->io_in);
+  if (G->io_out) cudaStreamDestroy(G->io_out);
+  for (cudaEvent_t e : G->io_ev)
+    if (e) cudaEventDestroy(e);
   double* ws[] = {G->w_x, G->w_f, G->w_r, G->w_p, G->w_q, G->w_z, G->w_t, G->w_d};
   for (double* w : ws) cudaFree(w);
   cudaFree(G->pcg_ctl);
@@ -315,6 +320,70 @@ vt_status vt_apply_projected(vt_grid* G, const double* scale, const double* u, d
                              void* stream) {
   return launch_hex8(G, H8_APPLY, false, scale, u, nullptr, nullptr, v, 0.0, nullptr, nullptr,
                      (cudaStream_t)stream);
+}
+
+// v = K(rho) u from host memory to host memory, streamed in z-chunks: the
+// H2D copy of chunk c+1 (copy engine 1), the operator on chunk c (SMs) and the
+// D2H copy of chunk c-1 (copy engine 2) overlap, so the call costs about one
+// PCIe transfer instead of two plus the kernel [ref: operator.py:154-165].
+// Host arrays are the reference's flat (n_dofs,) order (pinned memory gives
+// full PCIe bandwidth; pageable works through the driver's staging).  Blocking.
+vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, double* hv,
+                        int nchunks, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const Geom& g = G->g;
+  const int nown = g.pB - g.pA;
+  const size_t row = (size_t)(g.nx + 1) * 3;              // doubles per dense node row
+  const size_t dplane = row * (g.ny + 1);                 // doubles per dense node plane
+  if (!G->io_stage) {
+    VT_CUDA(cudaMalloc(&G->io_stage, (size_t)nown * dplane * sizeof(double)));
+    VT_TRY(alloc_vec(G, &G->io_raw));
+    VT_TRY(alloc_vec(G, &G->io_proj));
+    VT_TRY(alloc_vec(G, &G->io_v));
+    VT_CUDA(cudaStreamCreateWithFlags(&G->io_in, cudaStreamNonBlocking));
+    VT_CUDA(cudaStreamCreateWithFlags(&G->io_out, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : G->io_ev) VT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int nch = nchunks < 1 ? 1 : nchunks;
+  if (nch > 16) nch = 16;
+  if (nch > nown) nch = nown;
+  std::vector<int> pb(nch + 1);
+  for (int c = 0; c <= nch; ++c) pb[c] = g.pA + (int)((long long)nown * c / nch);
+  cudaEvent_t* ev_in = G->io_ev;
+  cudaEvent_t* ev_k = G->io_ev + 16;
+  cudaEvent_t ev_done = G->io_ev[32];
+  const double* hsrc = hu + (size_t)g.k0 * dplane;
+  double* hdst = hv + (size_t)g.k0 * dplane;
+  // the copy streams must not run ahead of work already queued on s
+  VT_CUDA(cudaEventRecord(ev_done, s));
+  VT_CUDA(cudaStreamWaitEvent(G->io_in, ev_done, 0));
+  VT_CUDA(cudaStreamWaitEvent(G->io_out, ev_done, 0));
+  for (int c = 0; c < nch; ++c) {
+    const size_t off = (size_t)(pb[c] - g.pA) * dplane;
+    const size_t cnt = (size_t)(pb[c + 1] - pb[c]) * dplane;
+    VT_CUDA(cudaMemcpyAsync(G->io_stage + off, hsrc + off, cnt * sizeof(double),
+                            cudaMemcpyHostToDevice, G->io_in));
+    VT_TRY(launch_unpack_project(G, G->io_stage + off, pb[c], pb[c + 1], G->io_raw, G->io_proj,
+                                 G->io_in));
+    VT_CUDA(cudaEventRecord(ev_in[c], G->io_in));
+  }
+  for (int c = 0; c < nch; ++c) {
+    // chunk c reads the first plane of chunk c+1 (its top neighbour)
+    VT_CUDA(cudaStreamWaitEvent(s, ev_in[c + 1 < nch ? c + 1 : c], 0));
+    VT_TRY(launch_hex8(G, H8_APPLY, false, scale, G->io_proj, G->io_raw, nullptr, G->io_v, 0.0,
+                       nullptr, nullptr, s, pb[c], pb[c + 1]));
+    VT_CUDA(cudaEventRecord(ev_k[c], s));
+    VT_CUDA(cudaStreamWaitEvent(G->io_out, ev_k[c], 0));
+    const size_t off = (size_t)(pb[c] - g.pA) * dplane;
+    VT_CUDA(cudaMemcpy2DAsync(hdst + off, row * sizeof(double), G->io_v + (size_t)pb[c] * g.nplane,
+                              (size_t)g.rp * 3 * sizeof(double), row * sizeof(double),
+                              (size_t)(pb[c + 1] - pb[c]) * (g.ny + 1), cudaMemcpyDeviceToHost,
+                              G->io_out));
+  }
+  VT_CUDA(cudaEventRecord(ev_done, G->io_out));
+  VT_CUDA(cudaStreamWaitEvent(s, ev_done, 0));
+  VT_CUDA(cudaStreamSynchronize(s));
+  return VT_OK;
 }
 
 vt_status vt_diagonal(vt_grid* G, const double* scale, double* d, void* stream) {

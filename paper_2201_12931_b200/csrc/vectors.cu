@@ -41,6 +41,38 @@ vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_
   return VT_OK;
 }
 
+// dense reference-order planes [pa, pb) (host order, first plane at `dense`)
+// -> vt layout: raw copy (identity values on fixed dofs) and the projected copy
+// the operator multiplies (fixed dofs zero) [ref: operator.py:71-81]
+__global__ void unpack_project_kernel(Geom g, const uint8_t* mask, const double* __restrict__ dense,
+                                      int pa, int pb, double* __restrict__ raw,
+                                      double* __restrict__ proj) {
+  const long long row = (long long)(g.nx + 1);
+  const long long nn = (long long)(pb - pa) * (g.ny + 1) * row;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % row);
+    const long long r = t / row;
+    const int j = (int)(r % (g.ny + 1));
+    const int p = (int)(r / (g.ny + 1)) + pa;
+    const long long node = ((long long)p * (g.ny + 1) + j) * g.rp + i;
+    const unsigned m = mask[(long long)p * g.mplane + (long long)j * g.mp + i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = dense[t * 3 + c];
+      raw[node * 3 + c] = v;
+      proj[node * 3 + c] = ((m >> c) & 1u) ? 0.0 : v;
+    }
+  }
+}
+vt_status launch_unpack_project(vt_grid* G, const double* dense, int pa, int pb, double* raw,
+                                double* proj, cudaStream_t s) {
+  unpack_project_kernel<<<G->nsm * 4, VT_THREADS, 0, s>>>(G->g, G->mask, dense, pa, pb, raw, proj);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 __global__ void zero_owned_kernel(Geom g, double* v) {
   long long b, e;
   owned_range(g, b, e);

@@ -83,6 +83,10 @@ struct vt_grid {
   const void* pcg_key[4] = {nullptr, nullptr, nullptr, nullptr};
   unsigned long long pcg_nodes = 0;   // kernel nodes per PCG iteration graph
   cudaStream_t stream = nullptr;      // private stream of the blocking solver
+  // streamed host-to-host apply (vt_apply_host): staging + copy streams
+  double *io_stage = nullptr, *io_raw = nullptr, *io_proj = nullptr, *io_v = nullptr;
+  cudaStream_t io_in = nullptr, io_out = nullptr;
+  cudaEvent_t io_ev[33] = {};
 
   long long vec_len() const { return (long long)g.P * g.nplane; }
   long long elem_len() const { return (long long)g.Q * g.eplane; }
@@ -111,12 +115,16 @@ const CUtensorMap* elem_map(vt_grid* G, const void* ptr);
 
 // kernel launchers (hex8_apply.cu)
 Hex8Launch hex8_plan(const Geom& g, int nsm);
+Hex8Launch hex8_plan_range(const Geom& g, int nsm, int nout);
 vt_status hex8_configure();
 vt_status launch_hex8(vt_grid* G, int mode, bool dot, const double* scale, const double* u,
                       const double* ufix, const double* f, double* out, double omega,
-                      double* partial, const int* stop, cudaStream_t s);
+                      double* partial, const int* stop, cudaStream_t s, int pbeg = -1,
+                      int pend = -1);
 // (vectors.cu)
 vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_t s);
+vt_status launch_unpack_project(vt_grid* G, const double* dense, int pa, int pb, double* raw,
+                                double* proj, cudaStream_t s);
 vt_status launch_dot(vt_grid* G, const double* x, const double* y, double* partial, int* nparts,
                      cudaStream_t s, const int* stop = nullptr);
 vt_status launch_sum_partials(const double* partial, int n, double* out, cudaStream_t s);

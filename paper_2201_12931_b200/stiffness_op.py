@@ -114,13 +114,34 @@ def from_device(dgrid: DeviceGrid, t: torch.Tensor, like) -> object:
     return dgrid.download(t)
 
 
+HOST_CHUNKS = 8  # z-chunks of the streamed host apply (H2D / kernel / D2H overlap)
+
+
+def _pinned_empty(n: int) -> np.ndarray:
+    """A fresh numpy array in page-locked memory (torch's caching host allocator)."""
+    return torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+
+
 def apply(state: OperatorState, u):
-    """v = K(rho) u (operator.py:154-165)."""
+    """v = K(rho) u (operator.py:154-165).
+
+    numpy in -> a new numpy array out, streamed through the GPU in z-chunks
+    (vt_apply_host: the host->device copy of the next chunk, the operator on
+    this one and the device->host copy of the previous one overlap); the
+    result lives in page-locked memory.  A DeviceVector stays on the device."""
     d = state.dgrid
-    ud = as_device(d, u)
-    v = d.zeros()
-    check(lib.vt_apply(d.handle, ptr(state.scale_dev), ptr(ud), ptr(v), stream_ptr()))
-    return from_device(d, v, u)
+    if isinstance(u, DeviceVector):
+        ud = as_device(d, u)
+        v = d.zeros()
+        check(lib.vt_apply(d.handle, ptr(state.scale_dev), ptr(ud), ptr(v), stream_ptr()))
+        return from_device(d, v, u)
+    a = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+    if a.shape != (d.n_dofs,):
+        raise ValueError(f"expected dof vector of length {d.n_dofs}")
+    out = _pinned_empty(d.n_dofs)
+    check(lib.vt_apply_host(d.handle, ptr(state.scale_dev), a.ctypes.data_as(C.c_void_p),
+                            out.ctypes.data_as(C.c_void_p), HOST_CHUNKS, stream_ptr()))
+    return out
 
 
 def diagonal(state: OperatorState):
