@@ -47,6 +47,8 @@ def _args():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--simp-iters", type=int, default=4, help="SIMP iterations timed for the solve figure")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--slabs", action="store_true",
+                    help="use the z-slab/NCCL path even at N=1 (under torchrun; smoke test of the transport)")
     return ap.parse_args()
 
 
@@ -133,16 +135,17 @@ def run_ours(a):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    slabs = world > 1 or a.slabs
+    if slabs:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
-        if world > 1:
+        if slabs:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
+        if not slabs:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -165,7 +168,7 @@ def run_ours(a):
     hbm_peak, peak_src = _peaks()
     solve = None
 
-    if world == 1:
+    if not slabs:
         # ---- value: device-resident K(rho)u (the operator CG applies every iteration)
         state = vb.OperatorState(grid, rho, problem.model, fm, problem.stiffness())
         d = state.dgrid
@@ -221,7 +224,7 @@ def run_ours(a):
     achieved = alg_bytes / t_step / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
-    if world == 1 and os.path.exists(tf):
+    if not slabs and os.path.exists(tf):
         try:
             traffic = json.load(open(tf)).get("dram_bytes_per_launch")
         except Exception:
@@ -240,7 +243,7 @@ def run_ours(a):
     assert out.shape == (n,)
 
     # ---- MGPCG solve per SIMP iteration
-    if a.simp_iters > 0 and world == 1:
+    if a.simp_iters > 0 and not slabs:
         opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
         R = DeviceRun(problem, opt, vb.SolverConfig(tolerance=1e-5), "homogenized", spec["levels"], 0.4)
         times, its = [], []
@@ -297,7 +300,7 @@ def run_ours(a):
         "e2e": {"value": n / t_e2e / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n,
                 "path": "paper_2201_12931_b200.apply(state, pinned numpy) -> numpy (vt_apply_host, "
-                        "z-chunked H2D/kernel/D2H overlap)" if world == 1 else
+                        "z-chunked H2D/kernel/D2H overlap)" if not slabs else
                         "SlabSolver.upload -> apply -> download (host numpy, per-rank planes)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -305,7 +308,7 @@ def run_ours(a):
     }
     if rank == 0 and world == 1 and not a.no_cpu:
         res["cpu_baseline"] = cpu_baseline(a.config, reps=2)
-    if world > 1:
+    if slabs:
         S.close()
         dist.destroy_process_group()
     if rank == 0:

@@ -176,7 +176,8 @@ class SlabSolver:
 
     def download(self, vecs: Sequence[torch.Tensor], out: Optional[np.ndarray] = None) -> np.ndarray:
         """Owned planes of the local slabs into a global (n_dofs,) array."""
-        out = np.zeros(self.grid.n_dofs) if out is None else out
+        if out is None:  # page-locked, zero outside this process's planes
+            out = torch.zeros(self.grid.n_dofs, dtype=torch.float64, pin_memory=True).numpy()
         for dg, v in zip(self.slab_grids, vecs):
             check(lib.vt_vec_download(dg.handle, ptr(v), out.ctypes.data_as(C.c_void_p), stream_ptr()))
         torch.cuda.current_stream().synchronize()

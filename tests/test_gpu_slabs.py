@@ -80,3 +80,36 @@ def test_slab_plan_of_baseline_configs():
     assert p.dist_level == 5 and p.bounds[1] == 32
     p = plan_slabs(384, 8, 8)
     assert p.dist_level == 4 and p.bounds[1] == 48
+
+
+def test_nccl_transport_single_rank_matches_single():
+    """The NCCL code path (library-owned communicator bootstrapped over a
+    torch.distributed group, all-gathers / broadcasts captured in the iteration
+    graph) at world size 1 -- the only size one GPU allows -- solves like the
+    single-slab path."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        case, grid, rho, rng = _setup(32, 16, 16, seed=3)
+        st = vb.OperatorState(grid, rho, vb.MaterialModel(), case.fixed_mask)
+        H = vb.build_hierarchy(grid, st, 4, scheme="homogenized")
+        f = case.f_ext.copy()
+        f[case.fixed_mask] = 0.0
+        cfg = vb.SolverConfig(tolerance=1e-8, max_iterations=300)
+        x_ref, rep_ref = vb.mgcg_solve(st, H, f, cfg=cfg)
+        S = SlabSolver.from_process_group(grid, case.fixed_mask, levels=4)
+        S.set_density(rho)
+        x, rep = S.mgcg_solve(S.upload(f), cfg=cfg)
+        assert rep.converged and rep.iterations == rep_ref.iterations
+        assert np.abs(S.download(x) - x_ref).max() <= 1e-10 * np.abs(x_ref).max()
+        S.close()
+    finally:
+        dist.destroy_process_group()
