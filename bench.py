@@ -261,20 +261,27 @@ def run_ours(a):
                  "note": "first SIMP iterations of the cfg design loop (refresh + homogenized MGPCG, "
                          "V(1,1), tol 1e-5, warm start)"}
     elif a.simp_iters > 0:
-        f = problem.boundary.external_force(grid)
-        f[fm] = 0.0
-        rho0 = np.full(nel, spec["volfrac"])
-        barrier()
-        ts = time.perf_counter()
-        S.set_density(rho0, problem.model)
-        x, rep = S.mgcg_solve(S.upload(f), cfg=vb.SolverConfig(tolerance=1e-5))
-        barrier()
-        t_solve = max_over_ranks(time.perf_counter() - ts)
-        solve = {"s_per_simp_iter": t_solve, "simp_iters": 1, "cg_iters": [rep.iterations],
-                 "ms_per_cg_iter": 1e3 * t_solve / max(1, rep.iterations), "levels": S.levels,
-                 "dist_level": S.plan.dist_level,
-                 "note": "SIMP iteration 1 system (uniform volfrac densities): refresh + slab MGPCG, "
-                         "tol 1e-5, max over ranks"}
+        # the same design iterations on the slabs (SlabRun: refresh + slab MGPCG, then the
+        # distributed sensitivities / filter / OC), time of the solve part, max over ranks
+        from paper_2201_12931_b200.slabs import SlabRun
+
+        opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
+        R = SlabRun.from_process_group(problem, opt, vb.SolverConfig(tolerance=1e-5), spec["levels"], 0.4)
+        times, its = [], []
+        for it in range(a.simp_iters):
+            barrier()
+            ts = time.perf_counter()
+            rep = R.solve(problem.model)
+            torch.cuda.synchronize()
+            times.append(max_over_ranks(time.perf_counter() - ts))
+            its.append(rep.iterations)
+            R.design_step(problem.model)
+        solve = {"s_per_simp_iter": sum(times) / len(times), "simp_iters": a.simp_iters, "cg_iters": its,
+                 "ms_per_cg_iter": 1e3 * sum(times) / max(1, sum(its)), "levels": R.S.levels,
+                 "dist_level": R.S.plan.dist_level,
+                 "note": "first SIMP iterations on z-slabs (refresh + slab MGPCG, V(1,1), tol 1e-5, warm "
+                         "start; design step distributed too), max over ranks"}
+        R.S.close()
 
     res = {
         "metric": METRIC,

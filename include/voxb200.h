@@ -241,6 +241,26 @@ vt_status vt_dist_vcycle(vt_dist *D, const double *const *f, double *const *z, v
 /* MGPCG over all ranks, same recurrences as vt_pcg [ref: solver.py:62-191]; blocking */
 vt_status vt_dist_pcg(vt_dist *D, const double *const *f, double *const *x, int warm, double tol,
                       int max_iterations, vt_solve_report *rep, void *stream);
+/* design step on the slabs [ref: optimize.py:139-302]: element fields are the
+ * plain slab ranges of the reference element order (slab i: layers
+ * [kbounds[rank], kbounds[rank+1])).  Sensitivities refresh u's ghost planes;
+ * the filter exchanges R element layers of rho*dc with each neighbour and is
+ * bit-identical to the single-GPU filter; OC bisection and change/volume sum
+ * per rank, all-gather and add in rank order (identical decisions on every
+ * rank).  oc_update / change_volume are blocking. */
+vt_status vt_dist_sensitivities(vt_dist *D, double *const *u, const double *const *rho, double p,
+                                double kmin, double E, int grav_axis, double grav_coef,
+                                double *const *dc, void *stream);
+vt_status vt_dist_filter_create(vt_dist *D, int R, const double *kernel_host);
+vt_status vt_dist_filter_apply(vt_dist *D, const double *const *dc, const double *const *rho,
+                               double gamma, double *const *dcf, void *stream);
+vt_status vt_dist_oc_update(vt_dist *D, const double *const *rho, const int8_t *const *classes,
+                            const double *const *dc, const double *const *dv, double volfrac,
+                            double move, double eta, double q, double *const *rho_out,
+                            double *lam, int *steps, void *stream);
+vt_status vt_dist_change_volume(vt_dist *D, const double *const *a, const double *const *b,
+                                const int8_t *const *classes, double *max_abs_diff,
+                                double *active_mean, void *stream);
 
 #ifdef __cplusplus
 }

@@ -34,36 +34,14 @@
 // arithmetic is identical.
 #include <dlfcn.h>
 #include <math.h>
-#include <nccl.h>
 #include <stdlib.h>
 #include <string.h>
 
-#include <string>
-#include <vector>
-
-#include "vt_internal.h"
-#include "vt_pcg.cuh"
+#include "dist_internal.h"
 
 namespace vt {
 
-// ------------------------------------------------------------------ NCCL (dlopen)
-struct NcclApi {
-  bool ok = false;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
-
-static NcclApi& nccl() {
+NcclApi& nccl() {
   static NcclApi api;
   static bool tried = false;
   if (tried) return api;
@@ -93,14 +71,6 @@ static NcclApi& nccl() {
   return api;
 }
 
-#define VT_NCCL(call)                                                                        \
-  do {                                                                                       \
-    ncclResult_t r_ = (call);                                                                \
-    if (r_ != ncclSuccess)                                                                   \
-      return ::vt::fail(VT_ECUDA, std::string("NCCL error ") +                               \
-                                      (nccl().GetErrorString ? nccl().GetErrorString(r_) : "") + \
-                                      " at " #call);                                         \
-  } while (0)
 
 // ------------------------------------------------------------------ kernels
 // one slab's CTA partials -> its rank slot (fixed order); `sel` picks the
@@ -114,41 +84,10 @@ __global__ void slab_sum_kernel(const PcgCtl* ctl, const double* partial, int n,
   if (threadIdx.x == 0) *out = s;
 }
 
-struct DSlab {
-  int rank = 0;
-  std::vector<vt_grid*> lv;                       // levels 0..D (slab geometry)
-  std::vector<double*> u, u2, r, f, scale, rho;   // per level; f[0] unused
-  double *x = nullptr, *fv = nullptr, *rr = nullptr, *p = nullptr, *q = nullptr, *t = nullptr;
-  const double* z = nullptr;                      // V-cycle output buffer (level 0)
-  int tkb = 0, tke = 0;                           // tail-level coarse planes restricted here
-};
-
-constexpr int NSLOT = 8;
 
 }  // namespace vt
 
-struct vt_dist {
-  int N = 1, rank0 = 0, nlocal = 1, L = 1, D = 0, device = 0, sweeps = 1;
-  double omega = 0.4;
-  int nx = 0, ny = 0, nz = 0;
-  std::vector<int> kb;                 // level-0 slab boundaries (N + 1)
-  std::vector<vt::DSlab> sl;           // slabs of this process
-  vt_grid* full = nullptr;             // replicated full grid of level D
-  vt_hier* tail = nullptr;             // levels D..L-1 on every rank
-  double* rho_full = nullptr;          // level-D densities, plain, full grid
-  double* scale_full = nullptr;        // level-D scale, vt element layout
-  double* scal = nullptr;              // device [NSLOT][N] per-rank scalars
-  double* host_scal = nullptr;         // pinned mirror
-  vt::PcgCtl* ctl = nullptr;
-  vt::PcgCtl* ctl_host = nullptr;      // pinned ring of 2
-  cudaGraphExec_t graph = nullptr;
-  unsigned long long nodes = 0;
-  cudaStream_t stream = nullptr;
-  ncclComm_t comm = nullptr;
-  bool refreshed = false;
 
-  bool remote() const { return comm != nullptr; }
-};
 
 namespace vt {
 
@@ -156,7 +95,7 @@ static int lvl_k(int k, int l) { return k >> l; }
 
 // ------------------------------------------------------------------ exchanges
 // ghost node planes of level l for one vector per local slab
-static vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStream_t s) {
+vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStream_t s) {
   if (D->N == 1) return VT_OK;
   if (!D->remote()) {
     for (int i = 0; i < D->N; ++i) {
@@ -192,7 +131,7 @@ static vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cu
 }
 
 // ghost element layer (q = 0) of level l: the neighbour below's top layer
-static vt_status halo_elems(vt_dist* D, int l, const std::vector<double*>& e, cudaStream_t s) {
+vt_status halo_elems(vt_dist* D, int l, const std::vector<double*>& e, cudaStream_t s) {
   if (D->N == 1) return VT_OK;
   if (!D->remote()) {
     for (int i = 1; i < D->N; ++i) {
@@ -214,14 +153,14 @@ static vt_status halo_elems(vt_dist* D, int l, const std::vector<double*>& e, cu
 }
 
 // per-rank scalar slot -> complete on every rank
-static vt_status gather_scal(vt_dist* D, int slot, cudaStream_t s) {
+vt_status gather_scal(vt_dist* D, int slot, cudaStream_t s) {
   if (!D->remote()) return VT_OK;
   double* base = D->scal + (size_t)slot * D->N;
   VT_NCCL(nccl().AllGather(base + D->sl[0].rank, base, 1, ncclDouble, D->comm, s));
   return VT_OK;
 }
 
-static vt_status slab_sum(vt_dist* D, int i, const double* partial, int n, int n50, int slot,
+vt_status slab_sum(vt_dist* D, int i, const double* partial, int n, int n50, int slot,
                           const PcgCtl* ctl, cudaStream_t s) {
   slab_sum_kernel<<<1, 32, 0, s>>>(ctl, partial, n, n50,
                                    D->scal + (size_t)slot * D->N + D->sl[i].rank);
@@ -231,7 +170,7 @@ static vt_status slab_sum(vt_dist* D, int i, const double* partial, int n, int n
 }
 
 // host-side sum of a complete slot in rank order (setup scalars only)
-static vt_status host_slot_sum(vt_dist* D, int slot, cudaStream_t s, double* out) {
+vt_status host_slot_sum(vt_dist* D, int slot, cudaStream_t s, double* out) {
   VT_TRY(gather_scal(D, slot, s));
   VT_CUDA(cudaMemcpyAsync(D->host_scal, D->scal + (size_t)slot * D->N, D->N * sizeof(double),
                           cudaMemcpyDeviceToHost, s));
@@ -239,6 +178,14 @@ static vt_status host_slot_sum(vt_dist* D, int slot, cudaStream_t s, double* out
   double acc = 0.0;
   for (int g = 0; g < D->N; ++g) acc += D->host_scal[g];
   *out = acc;
+  return VT_OK;
+}
+
+vt_status host_slot_values(vt_dist* D, int slot, cudaStream_t s, double* out) {
+  VT_TRY(gather_scal(D, slot, s));
+  VT_CUDA(cudaMemcpyAsync(out, D->scal + (size_t)slot * D->N, D->N * sizeof(double),
+                          cudaMemcpyDeviceToHost, s));
+  VT_CUDA(cudaStreamSynchronize(s));
   return VT_OK;
 }
 
@@ -568,6 +515,9 @@ vt_status vt_dist_destroy(vt_dist* D) {
   if (D->full) vt_grid_destroy(D->full);
   cudaFree(D->rho_full); cudaFree(D->scale_full); cudaFree(D->scal); cudaFreeHost(D->host_scal);
   cudaFree(D->ctl); cudaFreeHost(D->ctl_host);
+  cudaFree(D->fw); cudaFree(D->opart);
+  for (double* p : D->fwsum) cudaFree(p);
+  for (double* p : D->fprod) cudaFree(p);
   if (D->comm) nccl().CommDestroy(D->comm);
   delete D;
   return VT_OK;

@@ -84,6 +84,17 @@ def initial_densities(regions: RegionMask, volfrac: float) -> DensityField:
 
 
 # ---------------------------------------------------------------- filter
+def filter_weights(h: float, radius: float):
+    """(R, (2R+1)^3 kernel in (dk, dj, di) order): conic weights r - dist on the
+    offset box, zero outside the radius (optimize.py:110-171)."""
+    R = int(np.floor(radius / h + 1e-12))
+    o = np.arange(-R, R + 1)
+    dk, dj, di = np.meshgrid(o, o, o, indexing="ij")
+    dist = h * np.sqrt(di**2 + dj**2 + dk**2)
+    inside = dist <= radius + 1e-12 * radius
+    return R, np.ascontiguousarray(np.where(inside, radius - dist, 0.0), dtype=np.float64)
+
+
 class FilterWeights:
     """Conic weights r - dist on the (2R+1)^3 offset box (optimize.py:110-171).
 

@@ -33,7 +33,7 @@ import torch
 from ._lib import SolveReportC, check, lib
 from .device import DeviceGrid, ptr, require_cuda, stream_ptr
 from .hierarchy import max_feasible_levels
-from .krylov import SolveReport, SolverConfig
+from .krylov import AUX_BUDGET_FACTOR, SolveReport, SolverConfig
 from .material import MaterialModel
 from .mesh import StructuredGrid, node_mask_bytes
 
@@ -229,6 +229,13 @@ class SlabSolver:
         """MGPCG over all ranks (solver.py:170-191 with the pcg of 62-167)."""
         if cfg.preconditioner != "multigrid":
             raise ValueError("the slab solver implements the multigrid preconditioner")
+        n = self.grid.n_dofs
+        aux = 4 * n + sum(5 * 3 * ((self.grid.nelx >> l) + 1) * ((self.grid.nely >> l) + 1) * ((self.grid.nelz >> l) + 1)
+                          for l in range(self.levels))
+        if aux > AUX_BUDGET_FACTOR * n:  # [ref: solver.py:183-187]
+            from .errors import SolverBreakdown
+
+            raise SolverBreakdown(f"auxiliary vector budget {aux} exceeds {AUX_BUDGET_FACTOR} * n")
         x = [t.clone() for t in u_prev] if (u_prev is not None and cfg.warm_start) else self.zeros()
         rep = SolveReportC()
         t0 = time.perf_counter()
@@ -237,5 +244,155 @@ class SlabSolver:
               "vt_dist_pcg")
         return x, SolveReport(iterations=rep.iterations, final_rel_residual=rep.final_rel_residual,
                               precond_applications=rep.precond_applications, wall_s=time.perf_counter() - t0,
-                              converged=bool(rep.converged), aux_vector_scalars=0,
+                              converged=bool(rep.converged), aux_vector_scalars=aux,
                               residual_drift=rep.residual_drift)
+
+
+# ---------------------------------------------------------------------------
+# the design loop on slabs
+class SlabRun:
+    """Device-resident SIMP loop over z-slabs (optimize.py:344-455): refresh +
+    slab MGPCG, compliance, sensitivities (u halo), filter (R-layer halos of
+    rho*dc), OC (rank-ordered sums per lambda step), change / volume.  Element
+    fields live as per-slab plain ranges of the reference element order."""
+
+    def __init__(self, problem, opt, solver: SolverConfig, max_levels=None, omega: float = 0.4,
+                 nranks: int = 1, rank: int = 0, nlocal: Optional[int] = None, nccl_id: Optional[bytes] = None,
+                 init_densities=None, group=None):
+        from .design import filter_weights, initial_densities
+
+        if problem.boundary.gravity is not None:
+            raise NotImplementedError("self-weight loads are not distributed yet; use run()")
+        if solver.preconditioner != "multigrid":
+            raise ValueError("the slab solver implements the multigrid preconditioner")
+        grid = problem.grid
+        self.problem, self.opt, self.solver, self.group = problem, opt, solver, group
+        fm = problem.boundary.fixed_mask(grid)
+        self.S = S = SlabSolver(grid, fm, max_levels, omega, nranks=nranks, rank=rank, nlocal=nlocal,
+                                nccl_id=nccl_id, nu=problem.nu)
+        f_ext = problem.boundary.external_force(grid)
+        f_ext[fm] = 0.0
+        self.f = S.upload(f_ext)
+        rho0 = (init_densities.values if init_densities is not None
+                else initial_densities(problem.regions, opt.volfrac).values)
+        self.rho = S._slab_rho(rho0)
+        self.rho = [r.clone() for r in self.rho]
+        self.rho_new = [torch.empty_like(r) for r in self.rho]
+        nxy = grid.nelx * grid.nely
+        cls = torch.as_tensor(np.ascontiguousarray(problem.regions.classes, dtype=np.int8),
+                              device=f"cuda:{S.device}")
+        self.cls = [cls[dg.k0 * nxy:dg.k1 * nxy].contiguous() for dg in S.slab_grids]
+        self.dv = [torch.ones_like(r) for r in self.rho]
+        self.dc = [torch.empty_like(r) for r in self.rho]
+        self.dcf = [torch.empty_like(r) for r in self.rho]
+        self.u = S.zeros()
+        R, kern = filter_weights(grid.h, opt.filter_radius)
+        check(lib.vt_dist_filter_create(S._h, R, kern.ctypes.data_as(C.c_void_p)), "vt_dist_filter_create")
+
+    @classmethod
+    def from_process_group(cls, problem, opt, solver, max_levels=None, omega=0.4, init_densities=None,
+                           group=None):
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [None]
+        if rank == 0:
+            n = int(lib.vt_nccl_id_bytes())
+            buf = (C.c_uint8 * n)()
+            check(lib.vt_nccl_unique_id(buf, n), "vt_nccl_unique_id")
+            obj[0] = bytes(buf)
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(problem, opt, solver, max_levels, omega, nranks=world, rank=rank, nlocal=1,
+                   nccl_id=obj[0], init_densities=init_densities, group=group)
+
+    def solve(self, model) -> SolveReport:
+        S = self.S
+        S.model = model
+        for dg, r, sc in zip(S.slab_grids, self.rho, S.scales):
+            check(lib.vt_scale_from_density(dg.handle, ptr(r), model.p, model.kmin_frac, model.E, ptr(sc),
+                                            stream_ptr()))
+        check(lib.vt_dist_refresh(S._h, _ptr_array(self.rho), _ptr_array(S.scales), model.p,
+                                  model.kmin_frac, model.E, stream_ptr()), "vt_dist_refresh")
+        self.u, rep = S.mgcg_solve(self.f, u_prev=self.u, cfg=self.solver)
+        return rep
+
+    def design_step(self, model):
+        """compliance, sensitivities, filter, OC; swaps rho. Returns (c, change, volume)."""
+        S, opt = self.S, self.opt
+        c = S.dot(self.f, self.u)
+        check(lib.vt_dist_sensitivities(S._h, _ptr_array(self.u), _ptr_array(self.rho), model.p,
+                                        model.kmin_frac, model.E, -1, 0.0, _ptr_array(self.dc), stream_ptr()))
+        check(lib.vt_dist_filter_apply(S._h, _ptr_array(self.dc), _ptr_array(self.rho), float(opt.gamma),
+                                       _ptr_array(self.dcf), stream_ptr()))
+        lam, steps = C.c_double(), C.c_int()
+        check(lib.vt_dist_oc_update(S._h, _ptr_array(self.rho), _ptr_array(self.cls), _ptr_array(self.dcf),
+                                    _ptr_array(self.dv), float(opt.volfrac), float(opt.move), float(opt.eta),
+                                    float(opt.q), _ptr_array(self.rho_new), C.byref(lam), C.byref(steps),
+                                    stream_ptr()))
+        ch, vol = C.c_double(), C.c_double()
+        check(lib.vt_dist_change_volume(S._h, _ptr_array(self.rho_new), _ptr_array(self.rho),
+                                        _ptr_array(self.cls), C.byref(ch), C.byref(vol), stream_ptr()))
+        self.rho, self.rho_new = self.rho_new, self.rho
+        return c, ch.value, vol.value
+
+    def _gather(self, parts: List[torch.Tensor]) -> torch.Tensor:
+        if self.S.nlocal == self.S.nranks:
+            return torch.cat(parts)
+        import torch.distributed as dist
+
+        out = [torch.empty_like(parts[0]) for _ in range(self.S.nranks)]
+        dist.all_gather(out, parts[0].contiguous(), group=self.group)
+        return torch.cat(out)
+
+    def densities(self) -> np.ndarray:
+        return self._gather(self.rho).cpu().numpy()
+
+    def displacement(self) -> np.ndarray:
+        out = self.S.download(self.u)
+        if self.S.nlocal != self.S.nranks:
+            import torch.distributed as dist
+
+            t = torch.from_numpy(np.array(out))
+            dist.all_reduce(t, group=self.group)  # disjoint owned planes: the sum assembles the field
+            out = t.numpy()
+        return out
+
+
+def run_slabs(problem, opt, solver: SolverConfig = SolverConfig(), max_levels=None, omega: float = 0.4,
+              nranks: int = 1, group=None, init_densities=None, start_iteration: int = 0, on_iteration=None):
+    """run() (optimize.py:323-455, homogenized scheme) on z-slabs: all `nranks`
+    slabs in this process, or -- with `group` -- one slab per rank of the group."""
+    from dataclasses import replace
+
+    from .design import DensityField, OptResult, RunRecord, VOLUME_TOL
+    from .errors import NumericalError
+
+    if group is not None:
+        R = SlabRun.from_process_group(problem, opt, solver, max_levels, omega, init_densities, group)
+    else:
+        R = SlabRun(problem, opt, solver, max_levels, omega, nranks=nranks, init_densities=init_densities)
+    records: List = []
+    converged = False
+    iteration = start_iteration
+    while iteration < opt.max_iterations:
+        t0 = time.perf_counter()
+        model_k = replace(problem.model, p=opt.penal_at(iteration))
+        rep = R.solve(model_k)
+        c, ch, vol = R.design_step(model_k)
+        iteration += 1
+        if abs(vol - opt.volfrac) > VOLUME_TOL:
+            raise NumericalError(f"volume constraint violated after update: {vol} vs {opt.volfrac}")
+        rec = RunRecord(iteration, c, vol, ch, rep.iterations, rep.final_rel_residual,
+                        time.perf_counter() - t0, rep.aux_vector_scalars)
+        records.append(rec)
+        if on_iteration is not None:
+            on_iteration(rec, DensityField(R.densities(), problem.regions), R.displacement())
+        obj_ok = True
+        if opt.obj_tol is not None and len(records) >= 2:
+            obj_ok = abs(records[-1].compliance - records[-2].compliance) <= opt.obj_tol
+        if ch <= opt.ch_tol and obj_ok:
+            converged = True
+            break
+    res = OptResult(DensityField(R.densities(), problem.regions), R.displacement(), records, converged, iteration)
+    R.S.close()
+    return res
