@@ -200,49 +200,75 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
 
 // u_f (+)= P u_c with fine fixed dofs zeroed in P u_c.  Per axis (z, y, x):
 //   even: dst = src[i/2];  odd: dst = 0.5 * (src[(i-1)/2] + src[(i+1)/2])
+// A CTA takes one coarse row pair unit (J, K): it stages the coarse rows
+// (J..J+1) x (K..K+1) in shared memory with coalesced loads and writes the
+// fine rows (2J..2J+1) x (2K..2K+1) with one thread per fine dof, so every
+// global access is contiguous (the node-per-thread gather was load-issue and
+// sector bound at 3 doubles per node).  Same z -> y -> x pass order and
+// rounding as the reference: bit-identical.  A slab produces exactly the fine
+// planes it owns (coarse plane K covers fine planes 2K, 2K+1).
 template <bool ADD>
 __global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double* __restrict__ uc,
                                double* __restrict__ uf, const int* stop) {
   if (stop && *(volatile const int*)stop) return;
-  const long long nn = owned_nodes(gf);
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
-       t += (long long)gridDim.x * blockDim.x) {
-    int p, j, i;
-    node_coords(gf, t, p, j, i);
-    const int k = p - 1 + gf.k0;
-    const long long fnode = node_off(gf, p, j, i);
-    const unsigned m = mf[mask_off(gf, p, j, i)];
-    const int kz0 = k >> 1, kz1 = (k + 1) >> 1;
-    const int jy0 = j >> 1, jy1 = (j + 1) >> 1;
-    const int ix0 = i >> 1, ix1 = (i + 1) >> 1;
-    const bool oz = k & 1, oy = j & 1, ox = i & 1;
+  extern __shared__ double sc[];                        // [kz][jy][cw]
+  const int fk0 = gf.k0 + gf.pA - 1;                    // first owned fine plane
+  const int fk1 = gf.k0 + gf.pB - 1;                    // one past the last
+  const int K0 = fk0 >> 1, K1 = ((fk1 - 1) >> 1) + 1;   // coarse planes covering them
+  const int cy = gc.ny + 1;
+  const int cw = (gc.nx + 1) * 3, fw = (gf.nx + 1) * 3;
+  const int units = (K1 - K0) * cy;
+  for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const int K = K0 + unit / cy, J = unit % cy;
+    const int J1 = J + 1 <= gc.ny ? J + 1 : J, Kp = K + 1 <= gc.nz ? K + 1 : K;
+    __syncthreads();
+    for (int t = threadIdx.x; t < 4 * cw; t += blockDim.x) {
+      const int q = t / cw, e = t - q * cw;
+      const int kk = (q >> 1) ? Kp : K, jj = (q & 1) ? J1 : J;
+      sc[t] = uc[node_off(gc, kk - gc.k0 + 1, jj, 0) * 3 + e];
+    }
+    __syncthreads();
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      auto Z = [&](int ix, int iy) {
-        const double a = uc[node_off(gc, kz0 - gc.k0 + 1, iy, ix) * 3 + c];
-        if (!oz) return a;
-        const double b = uc[node_off(gc, kz1 - gc.k0 + 1, iy, ix) * 3 + c];
-        return 0.5 * __dadd_rn(a, b);
-      };
-      auto Y = [&](int ix) {
-        const double a = Z(ix, jy0);
-        if (!oy) return a;
-        return 0.5 * __dadd_rn(a, Z(ix, jy1));
-      };
-      double v = Y(ix0);
-      if (ox) v = 0.5 * __dadd_rn(v, Y(ix1));
-      if ((m >> c) & 1u) v = 0.0;
-      if (ADD)
-        uf[fnode * 3 + c] = __dadd_rn(uf[fnode * 3 + c], v);
-      else
-        uf[fnode * 3 + c] = v;
+    for (int c = 0; c < 2; ++c) {
+      const int fk = 2 * K + c;
+      if (fk < fk0 || fk >= fk1) continue;
+      const int pf = fk - gf.k0 + 1;
+#pragma unroll
+      for (int b2 = 0; b2 < 2; ++b2) {
+        const int fj = 2 * J + b2;
+        if (fj > gf.ny) continue;
+        double* row = uf + node_off(gf, pf, fj, 0) * 3;
+        const uint8_t* mrow = mf + mask_off(gf, pf, fj, 0);
+        for (int d = threadIdx.x; d < fw; d += blockDim.x) {
+          const int i = d / 3, comp = d - 3 * i;
+          const int I = i >> 1;
+          auto Y = [&](int ix) {
+            double z0 = sc[(0 * 2 + 0) * cw + ix * 3 + comp];
+            double z1 = sc[(0 * 2 + 1) * cw + ix * 3 + comp];
+            if (c) {  // z pass
+              z0 = 0.5 * __dadd_rn(z0, sc[(1 * 2 + 0) * cw + ix * 3 + comp]);
+              z1 = 0.5 * __dadd_rn(z1, sc[(1 * 2 + 1) * cw + ix * 3 + comp]);
+            }
+            return b2 ? 0.5 * __dadd_rn(z0, z1) : z0;  // y pass
+          };
+          double v = Y(I);
+          if (i & 1) v = 0.5 * __dadd_rn(v, Y(I + 1));  // x pass
+          if ((mrow[i] >> comp) & 1u) v = 0.0;
+          if (ADD)
+            row[d] = __dadd_rn(row[d], v);
+          else
+            row[d] = v;
+        }
+      }
     }
   }
 }
 
+static size_t prolong_smem(const Geom& gc) { return (size_t)4 * (gc.nx + 1) * 3 * sizeof(double); }
+
 vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
                              const int* stop, cudaStream_t s) {
-  prolong_kernel<true><<<F->nsm * 8, MG_THREADS, 0, s>>>(C->g, F->g, F->mask, uc, uf, stop);
+  prolong_kernel<true><<<F->nsm * 8, MG_THREADS, prolong_smem(C->g), s>>>(C->g, F->g, F->mask, uc, uf, stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -440,7 +466,7 @@ vt_status launch_coarse_solve(vt_hier* H, const double* f, double* u, const int*
   vt_grid* G = H->lv.back();
   const int n = H->nL;
   const size_t sm = (size_t)n * sizeof(double);
-  const int grid = (n + 255) / 256 > 32 ? 32 : (n + 255) / 256;
+  const int grid = (n + 7) / 8;  // one warp per row, 8 warps per CTA
   double *cf = H->cvec, *x0 = H->cvec + n, *cr = H->cvec + 2 * n;
   coarse_mv_kernel<0><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->Kinv, f, cf, x0, cr, u, stop);
   coarse_mv_kernel<1><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->A0, f, cf, x0, cr, u, stop);
@@ -491,7 +517,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
   }
   for (int l = L - 2; l >= top; --l) {
     vt_grid* G = H->lv[l];
-    prolong_kernel<true><<<G->nsm * 8, MG_THREADS, 0, s>>>(H->lv[l + 1]->g, G->g, G->mask,
+    prolong_kernel<true><<<G->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s>>>(H->lv[l + 1]->g, G->g, G->mask,
                                                            ucur[l + 1], ucur[l], stop);
     count_launch();
     VT_CUDA(cudaGetLastError());
@@ -681,7 +707,7 @@ vt_status vt_hier_prolong(vt_hier* H, int l, const double* coarse, double* fine,
   cudaStream_t s = (cudaStream_t)stream;
   if (l < 0 || l + 1 >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
   vt_grid* F = H->lv[l];
-  prolong_kernel<false><<<F->nsm * 8, MG_THREADS, 0, s>>>(H->lv[l + 1]->g, F->g, F->mask, coarse,
+  prolong_kernel<false><<<F->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s>>>(H->lv[l + 1]->g, F->g, F->mask, coarse,
                                                           fine, nullptr);
   count_launch();
   VT_CUDA(cudaGetLastError());
