@@ -174,22 +174,40 @@ vt_status launch_diag(vt_grid* G, const double* scale, double* d, cudaStream_t s
 // u = omega * (f / d) on free dofs, 0 on fixed: the first pre-smoothing sweep
 // from a zero iterate, bit-identical to the reference's
 // u += omega * ((f - K 0) / d) [ref: multigrid.py:387-393, 423-424].
+// One thread per node pair (i, i+1), i even: the row pitch is even, so the
+// pair's 6 doubles are 16-byte aligned and move as 3 vector loads / stores
+// (scalar per-node access was L2-request bound at 3 doubles per node).
 __global__ void jacobi0_kernel(Geom g, const uint8_t* mask, const double* scale, double kd,
                                double omega, const double* f, double* u, const int* stop) {
   if (stop && *(volatile const int*)stop) return;
-  const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
+  const int hp = (g.nx + 2) / 2;  // node pairs per row (last may hold the pad node)
+  const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * hp;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t % (g.nx + 1));
-    const long long r = t / (g.nx + 1);
+    const int i = 2 * (int)(t % hp);
+    const long long r = t / hp;
     const int j = (int)(r % (g.ny + 1));
     const int p = (int)(r / (g.ny + 1)) + g.pA;
     const long long node = node_off(g, p, j, i);
-    const unsigned m = mask[mask_off(g, p, j, i)];
-    const double d = node_diag(g, scale, p, j, i, kd);
+    const unsigned m2 = *reinterpret_cast<const uint16_t*>(mask + mask_off(g, p, j, i));
+    const double d0 = node_diag(g, scale, p, j, i, kd);
+    const bool two = i + 1 <= g.nx;
+    const double d1 = two ? node_diag(g, scale, p, j, i + 1, kd) : 1.0;
+    const double2* fv = reinterpret_cast<const double2*>(f + node * 3);
+    const double2 a = fv[0], b = fv[1], c = fv[2];
+    const double fin[6] = {a.x, a.y, b.x, b.y, c.x, c.y};
+    double o[6];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      u[node * 3 + c] = ((m >> c) & 1u) ? 0.0 : __dmul_rn(omega, __ddiv_rn(f[node * 3 + c], d));
+    for (int q = 0; q < 6; ++q) {
+      const int nd = q / 3, comp = q % 3;
+      const unsigned m = (m2 >> (8 * nd)) & 0xffu;
+      const double d = nd ? d1 : d0;
+      o[q] = ((m >> comp) & 1u) || (nd && !two) ? 0.0 : __dmul_rn(omega, __ddiv_rn(fin[q], d));
+    }
+    double2* uv = reinterpret_cast<double2*>(u + node * 3);
+    uv[0] = make_double2(o[0], o[1]);
+    uv[1] = make_double2(o[2], o[3]);
+    uv[2] = make_double2(o[4], o[5]);
   }
 }
 
