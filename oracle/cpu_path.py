@@ -218,6 +218,7 @@ class Lvl:
     fixed: np.ndarray
     k0: Optional[np.ndarray] = None
     scale: Optional[np.ndarray] = None
+    mats: Optional[np.ndarray] = None  # galerkin coarse levels (nel, 24, 24)
     diag: Optional[np.ndarray] = None
     u: Optional[np.ndarray] = None
     f: Optional[np.ndarray] = None
@@ -236,14 +237,126 @@ class Hier:
     omega: float
     sweeps: int
     chol: object = None
+    scheme: str = "homogenized"
+    gstack: Optional[np.ndarray] = None   # galerkin: W_c^T K0 W_c, c = 0..7
+    aff: Optional[tuple] = None           # galerkin: (coarse elem, octant, correction)
 
     @property
     def vector_scalars(self):
         return sum(5 * lv.n for lv in self.levels)
 
 
-def hier_build(es, h, fixed_mask, max_levels, omega=0.4, sweeps=1) -> Hier:
-    """Level grids and masks (multigrid.py:462-499), homogenized scheme only."""
+# ---- Galerkin scheme (multigrid.py:59-81, 216-278)
+def octant_weights(c: int) -> np.ndarray:
+    """Trilinear weights of the 8 coarse corners at the fine corners of octant c
+    (multigrid.py:59-70)."""
+    off = np.array([[x & 1, (x >> 1) & 1, (x >> 2) & 1] for x in range(8)], dtype=np.float64)
+    T = np.ones((8, 8))
+    for a in range(8):
+        pos = (off[c] + off[a]) / 2.0
+        for b in range(8):
+            w = 1.0
+            for d in range(3):
+                w *= pos[d] if off[b][d] else 1.0 - pos[d]
+            T[a, b] = w
+    return T
+
+
+GAL_W = np.zeros((8, 24, 24))
+for _c in range(8):
+    _T = octant_weights(_c)
+    for _ax in range(3):
+        GAL_W[_c, _ax::3, _ax::3] = _T
+del _c, _T, _ax
+
+
+def octant_groups(arr, coarse_es, trailing=()):
+    """(nel_coarse, 8, *trailing), octant = child corner index (multigrid.py:94-104)."""
+    cz, cy, cx = coarse_es
+    a = arr.reshape(cz, 2, cy, 2, cx, 2, *trailing)
+    a = np.moveaxis(a, (1, 3, 5), (3, 4, 5))
+    return a.reshape(cz * cy * cx, 8, *trailing)
+
+
+def free24(mask, es):
+    """(nel, 24) float mask: 1 on free local dofs (multigrid.py:144-147)."""
+    return gather((~np.asarray(mask, bool)).astype(np.float64), es)
+
+
+def galerkin_setup(H: "Hier", k0):
+    """Static data: G_c = W_c^T K0 W_c and the fine fixed-dof corrections
+    s_e W_c^T (K0 o mm^T - K0) W_c of elements touching a fixed dof
+    (multigrid.py:216-223, 235-260)."""
+    H.gstack = np.stack([GAL_W[c].T @ k0 @ GAL_W[c] for c in range(8)])
+    fine, coarse = H.levels[0], H.levels[1]
+    groups = octant_groups(free24(fine.mask, fine.es), coarse.es, (24,))
+    pairs = np.argwhere(groups.min(axis=2) < 0.5)
+    if pairs.size == 0:
+        H.aff = None
+        return
+    E, C = pairs[:, 0], pairs[:, 1]
+    m = groups[E, C]
+    delta = k0[None, :, :] * (m[:, :, None] * m[:, None, :]) - k0[None, :, :]
+    H.aff = (E, C, np.matmul(np.swapaxes(GAL_W[C], 1, 2), np.matmul(delta, GAL_W[C])))
+
+
+def galerkin_level1(H: "Hier", scale0):
+    """Level-1 element matrices sum_c s_c G_c (+ corrections) (multigrid.py:262-270)."""
+    s_oct = octant_groups(scale0, H.levels[1].es)
+    KE = (s_oct @ H.gstack.reshape(8, 576)).reshape(-1, 24, 24)
+    if H.aff is not None:
+        E, C, corr = H.aff
+        np.add.at(KE, E, s_oct[E, C][:, None, None] * corr)
+    return KE
+
+
+def galerkin_coarsen(lv: Lvl, coarse_es):
+    """sum_c W_c^T (K_child o mm^T) W_c (multigrid.py:272-278)."""
+    m = free24(lv.mask, lv.es)
+    kproj = lv.mats * (m[:, :, None] * m[:, None, :])
+    groups = octant_groups(kproj, coarse_es, (24, 24))
+    KE = np.zeros((groups.shape[0], 24, 24))
+    for c in range(8):
+        KE += np.matmul(GAL_W[c].T, np.matmul(groups[:, c], GAL_W[c]))
+    return KE
+
+
+def apply_mats(u, es, fixed_idx, mats):
+    """operator.py:58-81 with elem_matrices."""
+    uw = u.copy()
+    uw[fixed_idx] = 0.0
+    ve = np.matmul(mats, gather(uw, es)[:, :, None])[:, :, 0]
+    out = scatter(ve, es)
+    out[fixed_idx] = u[fixed_idx]
+    return out
+
+
+def diag_mats(es, fixed_idx, mats):
+    """operator.py:84-105 with elem_matrices."""
+    nz, ny, nx = es
+    out = np.zeros((nz + 1, ny + 1, nx + 1, 3))
+    ediag = np.einsum("eii->ei", mats).reshape(nz, ny, nx, 24)
+    for c in range(8):
+        _corner(out, c, es)[...] += ediag[..., 3 * c:3 * c + 3]
+    d = out.reshape(-1)
+    d[fixed_idx] = 1.0
+    return d
+
+
+def dense_mats(es, fixed_idx, mats):
+    nz, ny, nx = es
+    n = 3 * (nx + 1) * (ny + 1) * (nz + 1)
+    edofs = dof_table(es)
+    K = np.zeros((n, n))
+    np.add.at(K, (edofs[:, :, None], edofs[:, None, :]), mats)
+    K[fixed_idx, :] = 0.0
+    K[:, fixed_idx] = 0.0
+    K[fixed_idx, fixed_idx] = 1.0
+    return K
+
+
+def hier_build(es, h, fixed_mask, max_levels, omega=0.4, sweeps=1, scheme="homogenized") -> Hier:
+    """Level grids and masks (multigrid.py:462-499)."""
     nz, ny, nx = es
     L = min(int(max_levels), feasible_levels(nx, ny, nz))
     lv, mask, cur, hh = [], np.asarray(fixed_mask, bool), tuple(es), h
@@ -255,27 +368,36 @@ def hier_build(es, h, fixed_mask, max_levels, omega=0.4, sweeps=1) -> Hier:
             hh = hh * 2
     for x in lv:
         x.u, x.f, x.r, x.tmp = (np.zeros(x.n) for _ in range(4))
-    return Hier(lv, float(omega), int(sweeps))
+    return Hier(lv, float(omega), int(sweeps), scheme=scheme)
 
 
 def hier_refresh(H: Hier, rho, scale0, k0, p, kmin, E):
-    """Homogenized refresh (multigrid.py:201-233) + coarsest factor (280-316)."""
+    """Homogenized / Galerkin refresh (multigrid.py:201-233) + coarsest factor (280-316)."""
     H.levels[0].scale = scale0
     H.levels[0].k0 = k0
-    r = rho
-    for l in range(1, len(H.levels)):
-        lv = H.levels[l]
-        r = octant_mean(r, lv.es)
-        lv.scale = E * simp(r, p, kmin)
-        lv.k0 = k0 * float(2**l)
+    if H.scheme == "homogenized":
+        r = rho
+        for l in range(1, len(H.levels)):
+            lv = H.levels[l]
+            r = octant_mean(r, lv.es)
+            lv.scale = E * simp(r, p, kmin)
+            lv.k0 = k0 * float(2**l)
+    elif len(H.levels) > 1:
+        if H.gstack is None:
+            galerkin_setup(H, k0)
+        H.levels[1].mats = galerkin_level1(H, scale0)
+        for l in range(1, len(H.levels) - 1):
+            H.levels[l + 1].mats = galerkin_coarsen(H.levels[l], H.levels[l + 1].es)
     for lv in H.levels:
-        lv.diag = diag_k(lv.es, lv.fixed, lv.k0, lv.scale)
+        lv.diag = diag_mats(lv.es, lv.fixed, lv.mats) if lv.mats is not None else \
+            diag_k(lv.es, lv.fixed, lv.k0, lv.scale)
     last = H.levels[-1]
     if last.n > 20_000:
         raise OracleError("setup", f"coarsest level has {last.n} dofs")
-    if len(H.levels) > 1 and last.fixed.size < 6:
+    if H.scheme == "homogenized" and len(H.levels) > 1 and last.fixed.size < 6:
         raise OracleError("setup", f"only {last.fixed.size} fixed dofs survive")
-    K = dense_k(last.es, last.fixed, last.k0, last.scale)
+    K = dense_mats(last.es, last.fixed, last.mats) if last.mats is not None else \
+        dense_k(last.es, last.fixed, last.k0, last.scale)
     try:
         H.chol = scipy.linalg.cho_factor(K, lower=True)
     except scipy.linalg.LinAlgError as exc:
@@ -335,6 +457,8 @@ def restrict(H: Hier, l: int, rf):
 
 def level_apply(H: Hier, l: int, u):
     lv = H.levels[l]
+    if lv.mats is not None:
+        return apply_mats(u, lv.es, lv.fixed, lv.mats)
     return apply_k(u, lv.es, lv.fixed, lv.k0, lv.scale)
 
 
@@ -645,8 +769,8 @@ class Rec:
 
 def run_design(case: Case, volfrac, rmin, iters, tol=1e-5, maxit=200, max_levels=None,
                omega=0.4, ch_tol=0.01, move=0.2, eta=0.5, q=1.0, gamma=1e-3,
-               rho0=None, u0=None, on_iter: Optional[Callable] = None):
-    """SIMP loop of optimize.py:344-455, homogenized MGPCG only."""
+               rho0=None, u0=None, on_iter: Optional[Callable] = None, scheme="homogenized"):
+    """SIMP loop of optimize.py:344-455 with MGPCG (homogenized or galerkin)."""
     es = case.es
     k0 = hex8_k0(case.nu, case.h)
     fixed = np.flatnonzero(case.fixed_mask)
@@ -677,7 +801,7 @@ def run_design(case: Case, volfrac, rmin, iters, tol=1e-5, maxit=200, max_levels
         scale = case.E * simp(rho, case.p, case.kmin)
         f = gravity_load(rho, es, grav, f_ext, fixed) if grav is not None else f_ext
         if H is None:
-            H = hier_build(es, case.h, case.fixed_mask, max_levels, omega)
+            H = hier_build(es, case.h, case.fixed_mask, max_levels, omega, scheme=scheme)
         hier_refresh(H, rho, scale, k0, case.p, case.kmin, case.E)
         n = f.shape[0]
         budget = 4 * n + H.vector_scalars

@@ -122,6 +122,47 @@ def gen_multigrid(vt):
     np.savez_compressed(os.path.join(OUT, "multigrid.npz"), **out)
 
 
+def gen_galerkin(vt):
+    """Galerkin scheme (the reference default, multigrid.py:59-81, 216-278):
+    per-level element matrices, diagonals, coarse operators, V-cycle, coarsest
+    solve, MGCG counts."""
+    rng = np.random.default_rng(91)
+    out = {}
+    for tag, dims, L in (("t", (8, 4, 4), 3), ("v", (16, 8, 8), 3), ("x", (12, 8, 4), 2)):
+        grid = vt.build_grid(*dims, 1.0)
+        rho = rng.uniform(0.05, 1.0, grid.n_elements)
+        st = vt.OperatorState(grid, rho, vt.MaterialModel(), face_mask(vt, grid))
+        hier = vt.build_hierarchy(grid, st, L, scheme="galerkin")
+        out[f"{tag}_dims"] = np.array(dims)
+        out[f"{tag}_rho"] = rho
+        out[f"{tag}_levels"] = hier.n_levels
+        for l, lv in enumerate(hier.levels):
+            out[f"{tag}_diag{l}"] = lv.diag
+            if lv.mats is not None:
+                out[f"{tag}_mats{l}"] = lv.mats
+        for l in range(1, hier.n_levels):
+            uc = rng.standard_normal(hier.levels[l].n_dofs)
+            out[f"{tag}_cu{l}"] = uc
+            out[f"{tag}_cv{l}"] = hier.coarse_apply(l, uc)
+        f = rng.standard_normal(grid.n_dofs)
+        f[st.fixed_idx] = 0.0
+        out[f"{tag}_f"] = f
+        out[f"{tag}_z"] = hier.v_cycle(f)
+        fL = rng.standard_normal(hier.levels[-1].n_dofs)
+        fL[hier.levels[-1].fixed_idx] = 0.0
+        out[f"{tag}_fL"] = fL
+        out[f"{tag}_uL"] = hier.coarse_solve(fL)
+        out[f"{tag}_vector_scalars"] = hier.vector_scalars
+        out[f"{tag}_operator_scalars"] = hier.operator_scalars
+        out[f"{tag}_factor_scalars"] = hier.factor_scalars
+        for ctag, tol, maxit in (("a", 1e-5, 200), ("b", 1e-10, 500)):
+            x, rep = vt.mgcg_solve(st, hier, f, None, vt.SolverConfig(tolerance=tol, max_iterations=maxit))
+            out[f"{tag}{ctag}_x"] = x
+            out[f"{tag}{ctag}_rep"] = np.array([rep.iterations, rep.final_rel_residual, rep.precond_applications,
+                                                float(rep.converged), rep.aux_vector_scalars])
+    np.savez_compressed(os.path.join(OUT, "galerkin.npz"), **out)
+
+
 def gen_pcg(vt):
     from voxtop.app.presets import instantiate
     from voxtop.solver import jacobi_preconditioner
@@ -258,6 +299,17 @@ def gen_traj(vt, which):
         opt = vt.OptConfig(volfrac=0.12, filter_radius=2.5 * h, max_iterations=30, ch_tol=1e-12)
         recs, snaps, wall, _ = _traj(vt, problem, opt, {30}, max_levels=3, tol=1e-10, maxit=1000)
         np.savez_compressed(os.path.join(OUT, "small_tight.npz"), recs=recs, **snaps)
+    if "galtraj" in which:
+        # the reference default scheme end to end: 16x8x8, 20 iterations at the
+        # default tolerance and converged to 1e-10
+        problem, _ = instantiate("cantilever", (16, 8, 8))
+        h = problem.grid.h
+        opt = vt.OptConfig(volfrac=0.12, filter_radius=1.5 * h, max_iterations=20, ch_tol=1e-12)
+        recs, snaps, wall, _ = _traj(vt, problem, opt, {20}, scheme="galerkin", max_levels=3)
+        recs_t, snaps_t, wall, _ = _traj(vt, problem, opt, {20}, scheme="galerkin", max_levels=3, tol=1e-10,
+                                         maxit=1000)
+        np.savez_compressed(os.path.join(OUT, "galerkin_traj.npz"), recs=recs, rho20=snaps["rho20"],
+                            recs_tight=recs_t, rho20_tight=snaps_t["rho20"])
     if "small" in which:
         # fast end-to-end trajectory for GPU parity (16x8x8 cantilever, 2.5h filter)
         problem, _ = instantiate("cantilever", (16, 8, 8))
@@ -305,13 +357,13 @@ def gen_traj(vt, which):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="k0,operator,multigrid,pcg,design,small,bridge,grav,cfg1")
+    ap.add_argument("--only", default="k0,operator,multigrid,galerkin,pcg,design,small,bridge,grav,cfg1,galtraj")
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     vt = _vt()
     which = set(a.only.split(","))
     for name, fn in (("k0", gen_k0), ("operator", gen_operator), ("multigrid", gen_multigrid),
-                     ("pcg", gen_pcg), ("design", gen_design)):
+                     ("galerkin", gen_galerkin), ("pcg", gen_pcg), ("design", gen_design)):
         if name in which:
             t = time.perf_counter()
             fn(vt)

@@ -196,3 +196,52 @@ def test_cfg1_trajectory_first_iterations():
     case = O.cantilever_case(48, 24, 24)
     rho, u, recs = O.run_design(case, 0.12, 1.5 * case.h, 5, max_levels=4, ch_tol=1e-12)
     _check_traj(recs, g["recs"][:5], g["rho5"], rho)
+
+
+def _ghier(g, tag):
+    dims = tuple(int(x) for x in g[f"{tag}_dims"])
+    es = (dims[2], dims[1], dims[0])
+    mask = face_fixed_mask(*dims)
+    rho = g[f"{tag}_rho"]
+    H = O.hier_build(es, 1.0, mask, int(g[f"{tag}_levels"]), scheme="galerkin")
+    k0 = O.hex8_k0(0.3, 1.0)
+    scale = O.simp(rho, 3.0, 1e-9)
+    O.hier_refresh(H, rho, scale, k0, 3.0, 1e-9, 1.0)
+    return H, es, mask, k0, scale
+
+
+@pytest.mark.parametrize("tag", ["t", "v", "x"])
+def test_galerkin_matches_reference(tag):
+    """Galerkin scheme (the reference default): element matrices of every coarse
+    level, diagonals, coarse operators, coarsest solve, V-cycle and MGCG."""
+    g = golden("galerkin.npz")
+    H, es, mask, k0, scale = _ghier(g, tag)
+    assert len(H.levels) == int(g[f"{tag}_levels"])
+    assert H.vector_scalars == int(g[f"{tag}_vector_scalars"])
+    for l, lv in enumerate(H.levels):
+        if l >= 1:
+            want = g[f"{tag}_mats{l}"]
+            assert np.abs(lv.mats - want).max() <= 1e-13 * np.abs(want).max()
+        assert rel_err(lv.diag, g[f"{tag}_diag{l}"]) <= 1e-13
+    for l in range(1, len(H.levels)):
+        assert rel_err(O.level_apply(H, l, g[f"{tag}_cu{l}"]), g[f"{tag}_cv{l}"]) <= 1e-13
+    assert rel_err(O.coarse_solve(H, g[f"{tag}_fL"]), g[f"{tag}_uL"]) <= 1e-11
+    assert rel_err(O.vcycle(H, g[f"{tag}_f"]), g[f"{tag}_z"]) <= 1e-11
+    fixed = np.flatnonzero(mask)
+    ap = lambda v: O.apply_k(v, es, fixed, k0, scale)
+    rs = lambda v, ff: O.resid_k(v, ff, es, fixed, k0, scale)
+    for ctag, tol, maxit in (("a", 1e-5, 200), ("b", 1e-10, 500)):
+        x, rep = O.pcg(ap, rs, lambda r: O.vcycle(H, r), g[f"{tag}_f"], None, fixed, tol, maxit)
+        want = g[f"{tag}{ctag}_rep"]
+        assert rep.iterations == int(want[0]) and bool(rep.converged) == bool(want[3])
+        assert rel_err(x, g[f"{tag}{ctag}_x"]) <= max(1e-9, 0.1 * tol)
+
+
+def test_galerkin_trajectory():
+    g = golden("galerkin_traj.npz")
+    case = O.cantilever_case(16, 8, 8)
+    rho, u, recs = O.run_design(case, 0.12, 1.5 * case.h, 20, max_levels=3, ch_tol=1e-12, scheme="galerkin")
+    _check_traj(recs, g["recs"], g["rho20"], rho)
+    rho, u, recs = O.run_design(case, 0.12, 1.5 * case.h, 20, tol=1e-10, maxit=1000, max_levels=3,
+                                ch_tol=1e-12, scheme="galerkin")
+    _check_traj(recs, g["recs_tight"], g["rho20_tight"], rho)
