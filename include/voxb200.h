@@ -126,6 +126,13 @@ vt_status vt_dot(vt_grid *g, const double *x, const double *y, double *out, void
 typedef struct vt_hier vt_hier;
 
 vt_status vt_hier_create(vt_hier **out, vt_grid *fine, int n_levels, double omega, int sweeps);
+/* scheme 0: homogenized (coarse operators E s(mean rho) K0(2^l h), rebuilt on
+ * the fly); scheme 1: galerkin, the reference default -- per-element 24x24
+ * coarse matrices P^T K P with the fixed-dof projection [ref: multigrid.py:
+ * 59-81, 216-278], stored on levels >= 1 (576 doubles per coarse element). */
+vt_status vt_hier_create_ex(vt_hier **out, vt_grid *fine, int n_levels, double omega, int sweeps,
+                            int scheme);
+int vt_hier_scheme(const vt_hier *H);
 vt_status vt_hier_destroy(vt_hier *H);
 int vt_hier_levels(const vt_hier *H);
 vt_grid *vt_hier_grid(vt_hier *H, int level);
@@ -146,6 +153,9 @@ vt_status vt_hier_level_diag(vt_hier *H, int l, double *d, void *stream);
 vt_status vt_hier_coarse_solve(vt_hier *H, const double *f, double *u, void *stream);
 /* device pointer to level-l element scale / plain density (vt layouts) */
 const double *vt_hier_level_scale(vt_hier *H, int l);
+/* galerkin: level-l element matrices (n_elements_l x 576, reference element
+ * order, row-major 24x24); NULL for homogenized hierarchies or l = 0 */
+const double *vt_hier_level_mats(vt_hier *H, int l);
 const double *vt_hier_level_rho(vt_hier *H, int l);
 
 /* ---------------------------------------------------------- solver

@@ -58,6 +58,9 @@ _SIGS = {
     "vt_dot": (I, [P, P, P, C.POINTER(D), P]),
     "vt_hier_create": (I, [C.POINTER(P), P, I, D, I]),
     "vt_hier_destroy": (I, [P]),
+    "vt_hier_create_ex": (I, [C.POINTER(P), P, I, D, I, I]),
+    "vt_hier_scheme": (I, [P]),
+    "vt_hier_level_mats": (P, [P, I]),
     "vt_hier_levels": (I, [P]),
     "vt_hier_grid": (P, [P, I]),
     "vt_hier_refresh": (I, [P, P, P, D, D, D, P]),

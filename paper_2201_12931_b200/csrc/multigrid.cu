@@ -316,22 +316,22 @@ vt_status launch_coarsen_rho(vt_grid* F, vt_grid* C, const double* rf, double* r
 // Dense assembly (identity on fixed), in-place Cholesky; one CTA.
 // [ref: multigrid.py:280-316]
 __global__ void __launch_bounds__(1024, 1)
-    coarse_factor_kernel(Geom g, const double* scale, const double* k0l, const uint8_t* mask,
-                         int n, double* A, double* A0, int* status) {
+    coarse_factor_kernel(Geom g, const double* scale, const double* k0l, const double* mats,
+                         const uint8_t* mask, int n, double* A, double* A0, int* status) {
   const int nx1 = g.nx + 1, ny1 = g.ny + 1;
   for (long long t = threadIdx.x; t < (long long)n * n; t += blockDim.x) A[t] = 0.0;
   __syncthreads();
   const int nel = g.nx * g.ny * g.nz;
   for (int e = 0; e < nel; ++e) {
     const int i = e % g.nx, j = (e / g.nx) % g.ny, k = e / (g.nx * g.ny);
-    const double s = scale[elem_off(g, k + 1, j, i)];
+    const double s = mats ? 0.0 : scale[elem_off(g, k + 1, j, i)];
     for (int t = threadIdx.x; t < 576; t += blockDim.x) {
       const int a = t / 24, b = t % 24;
       const int ca = a / 3, cb = b / 3;
       const int na = (i + (ca & 1)) + (j + ((ca >> 1) & 1)) * nx1 + (k + (ca >> 2)) * nx1 * ny1;
       const int nb = (i + (cb & 1)) + (j + ((cb >> 1) & 1)) * nx1 + (k + (cb >> 2)) * nx1 * ny1;
       const int da = 3 * na + a % 3, db = 3 * nb + b % 3;
-      A[(long long)da * n + db] += s * k0l[t];
+      A[(long long)da * n + db] += mats ? mats[(long long)e * 576 + t] : s * k0l[t];
     }
     __syncthreads();
   }
@@ -481,7 +481,6 @@ vt_status hier_alloc_vec(vt_grid* G, double** p) {
   return VT_OK;
 }
 
-void hex8_k0_host(double nu, double h, double* K);  // runtime.cu
 
 // coarsest solve with one refinement step (3 launches, capturable)
 vt_status launch_coarse_solve(vt_hier* H, const double* f, double* u, const int* stop,
@@ -510,11 +509,16 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
   std::vector<double*> ucur(L);
   for (int l = 1; l < L; ++l) fl[l] = H->f[l];
   fl[top] = f0;
+  const auto gal = [&](int l) { return H->scheme == 1 && l >= 1; };  // stored-matrix level
   auto smooth = [&](int l, bool dot) -> vt_status {
     vt_grid* G = H->lv[l];
     double* dst = (ucur[l] == H->u[l]) ? H->u2[l] : H->u[l];
-    VT_TRY(launch_hex8(G, H8_SMOOTH, dot, H->scale[l], ucur[l], nullptr, fl[l], dst, H->omega,
-                       rz_partial, stop, s));
+    if (gal(l)) {
+      VT_TRY(gal_level_op(H, l, 2, ucur[l], fl[l], dst, stop, s));
+    } else {
+      VT_TRY(launch_hex8(G, H8_SMOOTH, dot, H->scale[l], ucur[l], nullptr, fl[l], dst, H->omega,
+                         rz_partial, stop, s));
+    }
     ucur[l] = dst;
     return VT_OK;
   };
@@ -522,10 +526,16 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
     vt_grid* G = H->lv[l];
     ucur[l] = H->u[l];
     if (H->sweeps >= 1) {
-      VT_TRY(launch_jacobi0(G, H->scale[l], H->omega, fl[l], H->u[l], stop, s));
+      if (gal(l))
+        VT_TRY(gal_jacobi0(H, l, fl[l], H->u[l], stop, s));
+      else
+        VT_TRY(launch_jacobi0(G, H->scale[l], H->omega, fl[l], H->u[l], stop, s));
       for (int k = 1; k < H->sweeps; ++k) VT_TRY(smooth(l, false));
-      VT_TRY(launch_hex8(G, H8_RESID, false, H->scale[l], ucur[l], ucur[l], fl[l], H->r[l], 0.0,
-                         nullptr, stop, s));
+      if (gal(l))
+        VT_TRY(gal_level_op(H, l, 1, ucur[l], fl[l], H->r[l], stop, s));
+      else
+        VT_TRY(launch_hex8(G, H8_RESID, false, H->scale[l], ucur[l], ucur[l], fl[l], H->r[l], 0.0,
+                           nullptr, stop, s));
       VT_TRY(launch_restrict(G, H->lv[l + 1], H->r[l], H->f[l + 1], stop, -1, -1, s));
     } else {
       VT_TRY(launch_zero_owned(G, H->u[l], s));
@@ -564,6 +574,12 @@ using namespace vt;
 extern "C" {
 
 vt_status vt_hier_create(vt_hier** out, vt_grid* fine, int n_levels, double omega, int sweeps) {
+  return vt_hier_create_ex(out, fine, n_levels, omega, sweeps, 0);
+}
+
+vt_status vt_hier_create_ex(vt_hier** out, vt_grid* fine, int n_levels, double omega, int sweeps,
+                            int scheme) {
+  if (scheme != 0 && scheme != 1) return fail(VT_EINVAL, "scheme must be 0 (homogenized) or 1 (galerkin)");
   if (!out || !fine) return fail(VT_EINVAL, "null argument");
   if (n_levels < 1) return fail(VT_EINVAL, "max_levels must be at least 1");
   if (!(omega > 0.0 && omega <= 1.0))
@@ -612,6 +628,12 @@ vt_status vt_hier_create(vt_hier** out, vt_grid* fine, int n_levels, double omeg
   }
   vt_grid* C = H->lv.back();
   H->nL = (int)(3LL * (C->g.nx + 1) * (C->g.ny + 1) * (C->g.nz + 1));
+  H->scheme = scheme;
+  if (scheme == 1) {
+    cudaDeviceSynchronize();  // coarse masks are built on the legacy stream
+    vt_status st = gal_setup(H);
+    if (st != VT_OK) { vt_hier_destroy(H); return st; }
+  }
   *out = H;
   return VT_OK;
 }
@@ -624,6 +646,7 @@ vt_status vt_hier_destroy(vt_hier* H) {
     cudaFree(H->scale[l]); cudaFree(H->rho[l]);
     if (l > 0) vt_grid_destroy(H->lv[l]);
   }
+  gal_free(H);
   cudaFree(H->A); cudaFree(H->A0); cudaFree(H->cvec); cudaFree(H->W); cudaFree(H->Kinv); cudaFree(H->k0l); cudaFree(H->status);
   delete H;
   return VT_OK;
@@ -634,6 +657,10 @@ vt_grid* vt_hier_grid(vt_hier* H, int l) {
   return (H && l >= 0 && l < (int)H->lv.size()) ? H->lv[l] : nullptr;
 }
 const double* vt_hier_level_scale(vt_hier* H, int l) { return H->scale[l]; }
+const double* vt_hier_level_mats(vt_hier* H, int l) {
+  return (H && H->scheme == 1 && l >= 1 && l < (int)H->lv.size()) ? H->mats[l] : nullptr;
+}
+int vt_hier_scheme(const vt_hier* H) { return H ? H->scheme : -1; }
 const double* vt_hier_level_rho(vt_hier* H, int l) { return H->rho[l]; }
 
 vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, double p,
@@ -647,13 +674,17 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
                           cudaMemcpyDeviceToDevice, s));
   int* bad = reinterpret_cast<int*>(F->scalars);
   VT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-  for (int l = 1; l < L; ++l) {
-    vt_grid* f = H->lv[l - 1];
-    vt_grid* c = H->lv[l];
-    coarsen_rho_kernel<<<c->nsm * 4, MG_THREADS, 0, s>>>(f->g.nx, f->g.ny, c->g.nx, c->g.ny,
-                                                         c->g.nz, H->rho[l - 1], H->rho[l]);
-    count_launch();
-    VT_TRY(launch_scale(c, H->rho[l], p, kmin, E, H->scale[l], bad, s));
+  if (H->scheme == 1) {
+    VT_TRY(gal_refresh(H, s));  // [ref: multigrid.py:216-223, 262-278]
+  } else {
+    for (int l = 1; l < L; ++l) {
+      vt_grid* f = H->lv[l - 1];
+      vt_grid* c = H->lv[l];
+      coarsen_rho_kernel<<<c->nsm * 4, MG_THREADS, 0, s>>>(f->g.nx, f->g.ny, c->g.nx, c->g.ny,
+                                                           c->g.nz, H->rho[l - 1], H->rho[l]);
+      count_launch();
+      VT_TRY(launch_scale(c, H->rho[l], p, kmin, E, H->scale[l], bad, s));
+    }
   }
   // coarsest direct factor
   vt_grid* C = H->lv.back();
@@ -661,7 +692,7 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
   if (n > 20000)
     return fail(VT_ESETUP, "coarsest level has " + std::to_string(n) +
                                " dofs, above the direct-solve guard 20000; increase the level count");
-  if (L > 1 && C->n_fixed < 6)
+  if (H->scheme == 0 && L > 1 && C->n_fixed < 6)
     return fail(VT_ESETUP, "only " + std::to_string(C->n_fixed) +
                                " fixed dofs survive on the coarsest level; rigid modes are "
                                "unconstrained (bad fixed-dof coarsening)");
@@ -686,8 +717,9 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
                                    (int)(n * sizeof(double))));
     }
   }
-  coarse_factor_kernel<<<1, 1024, 0, s>>>(C->g, H->scale[L - 1], H->k0l, C->mask, n, H->A,
-                                          H->A0, H->status);
+  coarse_factor_kernel<<<1, 1024, 0, s>>>(C->g, H->scale[L - 1], H->k0l,
+                                          (H->scheme == 1 && L > 1) ? H->mats[L - 1] : nullptr,
+                                          C->mask, n, H->A, H->A0, H->status);
   tri_inverse_kernel<<<(n + 127) / 128, 128, 0, s>>>(n, H->A, H->W);
   gram_kernel<<<C->nsm * 4, 256, 0, s>>>(n, H->W, H->Kinv);
   count_launch(3);
@@ -746,6 +778,11 @@ vt_status vt_hier_jacobi(vt_hier* H, int l, const double* u, const double* f, in
   const size_t bytes = G->vec_len() * sizeof(double);
   VT_CUDA(cudaMemcpyAsync(out, u, bytes, cudaMemcpyDeviceToDevice, s));
   for (int k = 0; k < sweeps; ++k) {
+    if (H->scheme == 1 && l >= 1) {
+      VT_TRY(gal_level_op(H, l, 2, out, f, G->scratch2, nullptr, s));
+      VT_CUDA(cudaMemcpyAsync(out, G->scratch2, bytes, cudaMemcpyDeviceToDevice, s));
+      continue;
+    }
     VT_TRY(launch_project(G, out, G->scratch, s));
     VT_TRY(launch_hex8(G, H8_SMOOTH, false, H->scale[l], G->scratch, out, f, G->scratch2,
                        H->omega, nullptr, nullptr, s));
@@ -756,11 +793,20 @@ vt_status vt_hier_jacobi(vt_hier* H, int l, const double* u, const double* f, in
 
 vt_status vt_hier_level_apply(vt_hier* H, int l, const double* u, double* v, void* stream) {
   if (l < 0 || l >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
+  if (H->scheme == 1 && l >= 1) {
+    if (!H->factored) return fail(VT_ESETUP, "hierarchy was not refreshed before use");
+    return gal_level_op(H, l, 0, u, nullptr, v, nullptr, (cudaStream_t)stream);
+  }
   return vt_apply(H->lv[l], H->scale[l], u, v, stream);
 }
 
 vt_status vt_hier_level_diag(vt_hier* H, int l, double* d, void* stream) {
   if (l < 0 || l >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
+  if (H->scheme == 1 && l >= 1) {
+    VT_CUDA(cudaMemcpyAsync(d, H->gdiag[l], H->lv[l]->vec_len() * sizeof(double),
+                            cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return VT_OK;
+  }
   return vt_diagonal(H->lv[l], H->scale[l], d, stream);
 }
 

@@ -106,6 +106,11 @@ struct vt_hier {
   int* status = nullptr;
   bool factored = false;
   const double* last_z = nullptr;  // buffer that holds the V-cycle output
+  // Galerkin scheme (galerkin.cu): scheme 1 stores per-element matrices on levels >= 1
+  int scheme = 0;                   // 0 homogenized, 1 galerkin
+  double *gG = nullptr, *gcorr = nullptr, *gve = nullptr;
+  int* gcorr_of = nullptr;
+  std::vector<double*> mats, gdiag;  // per level (index >= 1)
 };
 
 namespace vt {
@@ -143,4 +148,12 @@ vt_status launch_scale(vt_grid* G, const double* rho, double p, double kmin, dou
                        double* scale, int* bad, cudaStream_t s);
 vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, const int* stop,
                           int kb, int ke, cudaStream_t s);
+void hex8_k0_host(double nu, double h, double* K);
+// (galerkin.cu)
+vt_status gal_setup(vt_hier* H);
+void gal_free(vt_hier* H);
+vt_status gal_refresh(vt_hier* H, cudaStream_t s);
+vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const double* f, double* out,
+                       const int* stop, cudaStream_t s);
+vt_status gal_jacobi0(vt_hier* H, int l, const double* f, double* u, const int* stop, cudaStream_t s);
 }  // namespace vt

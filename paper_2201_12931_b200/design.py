@@ -299,11 +299,9 @@ class DeviceRun:
     def __init__(self, problem: Problem, opt: OptConfig, solver: SolverConfig, scheme: str,
                  max_levels: Optional[int], omega: float, init_densities=None, init_displacement=None):
         require_cuda()
-        if solver.preconditioner == "multigrid" and scheme != "homogenized":
-            if scheme not in ("galerkin", "homogenized"):
-                raise ValueError(f"unknown scheme {scheme!r}")
-            raise NotImplementedError(
-                "scheme='galerkin' is not implemented on the B200 path yet; use scheme='homogenized'")
+        if scheme not in ("galerkin", "homogenized"):
+            raise ValueError(f"unknown scheme {scheme!r}")
+        self.scheme = scheme
         grid = problem.grid
         self.problem, self.opt, self.solver = problem, opt, solver
         self.omega = omega
@@ -356,7 +354,7 @@ class DeviceRun:
         if sv.preconditioner == "multigrid":
             if self.hier is None:
                 self.hier = build_hierarchy(self.problem.grid, self.state_view(model), self.max_levels,
-                                            scheme="homogenized", omega=self.omega)
+                                            scheme=self.scheme, omega=self.omega)
             else:
                 self.hier._refresh_raw(self.rho, self.scale, model)
             aux = 4 * d.n_dofs + self.hier.vector_scalars
@@ -411,8 +409,9 @@ def run(problem: Problem, opt: OptConfig, solver: SolverConfig = SolverConfig(),
         on_iteration: Optional[Callable[[RunRecord, DensityField, np.ndarray], None]] = None) -> OptResult:
     """The SIMP loop (optimize.py:344-455) with every kernel on the device.
 
-    Same signature as the reference; the reference's default scheme is
-    "galerkin", which is not on the B200 path yet -- pass scheme="homogenized"."""
+    Same signature and defaults as the reference (scheme="galerkin" stores the
+    Galerkin coarse element matrices on the device; "homogenized" rebuilds the
+    coarse operators from averaged densities)."""
     R = DeviceRun(problem, opt, solver, scheme, max_levels, omega, init_densities, init_displacement)
     records: List[RunRecord] = []
     converged = False

@@ -1,9 +1,14 @@
-"""Homogenized geometric multigrid on the device -- drop-in for
-multigrid.py:84-499 of the reference (homogenized scheme).
+"""Geometric multigrid on the device -- drop-in for multigrid.py:84-499 of
+the reference, both coarse-operator schemes:
 
-Coarse operators are rebuilt on the fly from averaged densities
-(E*s(mean rho) * K0(h*2^l)); transfers, damped Jacobi and the V-cycle run as
-sm_100a kernels, the coarsest level is factored and inverted on the device.
+  * "galerkin" (the reference default): per-element 24x24 coarse matrices
+    P^T K P with the fixed-dof projection, assembled on the device from the
+    fine scales (level 1) and from the level below (csrc/galerkin.cu);
+  * "homogenized": coarse operators rebuilt on the fly from averaged densities
+    (E*s(mean rho) * K0(h*2^l)).
+
+Transfers, damped Jacobi and the V-cycle run as sm_100a kernels, the
+coarsest level is factored and inverted on the device.
 """
 
 from __future__ import annotations
@@ -65,6 +70,17 @@ class _Level:
         return d.elem_to_plain(t).cpu().numpy()
 
     @property
+    def mats(self) -> Optional[np.ndarray]:
+        """Galerkin element matrices (n_elements, 24, 24) of this level, else None."""
+        src = lib.vt_hier_level_mats(self.hier._h, self.index)
+        if not src:
+            return None
+        n = self.grid.n_elements * 576
+        t = torch.empty(n, dtype=torch.float64, device=f"cuda:{self.dgrid.device}")
+        check(lib.vt_copy(ptr(t), C.c_void_p(src), n * 8, stream_ptr()))
+        return t.cpu().numpy().reshape(-1, 24, 24)
+
+    @property
     def diag(self) -> np.ndarray:
         out = self.dgrid.zeros()
         check(lib.vt_hier_level_diag(self.hier._h, self.index, ptr(out), stream_ptr()))
@@ -82,7 +98,8 @@ class MgHierarchy:
         self.model = model
         self._fine = fine
         self._h = C.c_void_p()
-        check(lib.vt_hier_create(C.byref(self._h), fine.handle, len(levels_geom), self.omega, self.nu_pre))
+        check(lib.vt_hier_create_ex(C.byref(self._h), fine.handle, len(levels_geom), self.omega, self.nu_pre,
+                                    1 if scheme == "galerkin" else 0))
         self.levels: List[_Level] = []
         for l, (g, mask) in enumerate(levels_geom):
             if l == 0:
@@ -113,7 +130,8 @@ class MgHierarchy:
 
     @property
     def operator_scalars(self) -> int:
-        return sum(lv.grid.n_elements for lv in self.levels[1:])
+        per = 24 * 24 if self.scheme == "galerkin" else 1
+        return sum(lv.grid.n_elements * per for lv in self.levels[1:])
 
     @property
     def factor_scalars(self) -> int:
@@ -209,9 +227,8 @@ def build_hierarchy(grid: StructuredGrid, state: OperatorState, max_levels: int,
                     nu_post: int = 1) -> MgHierarchy:
     """Validate, build levels and refresh (multigrid.py:462-499).
 
-    Only scheme="homogenized" runs on the device in this release; the
-    Galerkin triple-product scheme (the reference default) is a SURVEY
-    section 8(f) "next" row and raises NotImplementedError."""
+    Both schemes run on the device; "galerkin" (the reference default)
+    stores 576 doubles per coarse element on levels >= 1."""
     if scheme not in SCHEMES:
         raise ValueError(f"unknown scheme {scheme!r}, expected one of {SCHEMES}")
     if not 0 < omega <= 1:
@@ -220,10 +237,6 @@ def build_hierarchy(grid: StructuredGrid, state: OperatorState, max_levels: int,
         raise ValueError("max_levels must be at least 1")
     if nu_pre != nu_post:
         raise ValueError("equal pre/post smoothing is required for a symmetric cycle")
-    if scheme == "galerkin":
-        raise NotImplementedError(
-            "scheme='galerkin' is not implemented on the B200 path yet; use scheme='homogenized'"
-        )
     L = min(int(max_levels), max_feasible_levels(grid.nelx, grid.nely, grid.nelz))
     geoms = []
     g, mask = grid, np.asarray(state.fixed_mask, dtype=bool)
