@@ -222,6 +222,7 @@ vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const do
 
 // ---------------------------------------------------------------- PCG passes
 // x += alpha p ; r -= alpha q ; partial ||r||^2   [ref: solver.py:131-136]
+// (16-byte vector accesses: owned ranges start and end on even indices)
 __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict__ x,
                                   const double* __restrict__ p, double* __restrict__ r,
                                   const double* __restrict__ q, double* partial, int with_r) {
@@ -234,14 +235,27 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
   const double alpha = ctl->alpha;
   long long b, e;
   owned_range(g, b, e);
+  double2* x2 = reinterpret_cast<double2*>(x + b);
+  const double2* p2 = reinterpret_cast<const double2*>(p + b);
+  double2* r2 = reinterpret_cast<double2*>(r + b);
+  const double2* q2 = reinterpret_cast<const double2*>(q + b);
+  const long long n2 = (e - b) / 2;
   double acc = 0.0;
-  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
        i += (long long)gridDim.x * blockDim.x) {
-    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double2 pv = p2[i];
+    double2 xv = x2[i];
+    xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+    xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+    x2[i] = xv;
     if (with_r) {
-      const double rv = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
-      r[i] = rv;
-      acc = fma(rv, rv, acc);
+      const double2 qv = q2[i];
+      double2 rv = r2[i];
+      rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, qv.x));
+      rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, qv.y));
+      r2[i] = rv;
+      acc = fma(rv.x, rv.x, acc);
+      acc = fma(rv.y, rv.y, acc);
     }
   }
   if (with_r) {
@@ -257,9 +271,17 @@ __global__ void pcg_xpby_kernel(Geom g, const PcgCtl* ctl, const double* __restr
   const double beta = ctl->beta;
   long long b, e;
   owned_range(g, b, e);
-  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
-       i += (long long)gridDim.x * blockDim.x)
-    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+  const double2* z2 = reinterpret_cast<const double2*>(z + b);
+  double2* p2 = reinterpret_cast<double2*>(p + b);
+  const long long n2 = (e - b) / 2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2 zv = z2[i];
+    double2 pv = p2[i];
+    pv.x = __dadd_rn(zv.x, __dmul_rn(beta, pv.x));
+    pv.y = __dadd_rn(zv.y, __dmul_rn(beta, pv.y));
+    p2[i] = pv;
+  }
 }
 
 // conditional copy dst = src (skip flag)
