@@ -259,7 +259,7 @@ vt_status vt_grid_destroy(vt_grid* G) {
   if (G->stream) cudaStreamDestroy(G->stream);
   cudaFree(G->mask); cudaFree(G->partial); cudaFree(G->scalars); cudaFreeHost(G->host_scalars);
   cudaFree(G->scratch); cudaFree(G->scratch2);
-  cudaFree(G->io_stage); cudaFree(G->io_raw); cudaFree(G->io_proj); cudaFree(G->io_v);
+  cudaFree(G->io_stage); cudaFree(G->io_stage_out); cudaFree(G->io_raw); cudaFree(G->io_proj); cudaFree(G->io_v);
   if (G->io_in) cudaStreamDestroy(G->io_in);
   if (G->io_out) cudaStreamDestroy(G->io_out);
   for (cudaEvent_t e : G->io_ev)
@@ -337,6 +337,7 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
   const size_t dplane = row * (g.ny + 1);                 // doubles per dense node plane
   if (!G->io_stage) {
     VT_CUDA(cudaMalloc(&G->io_stage, (size_t)nown * dplane * sizeof(double)));
+    VT_CUDA(cudaMalloc(&G->io_stage_out, (size_t)nown * dplane * sizeof(double)));
     VT_TRY(alloc_vec(G, &G->io_raw));
     VT_TRY(alloc_vec(G, &G->io_proj));
     VT_TRY(alloc_vec(G, &G->io_v));
@@ -368,17 +369,23 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
     VT_CUDA(cudaEventRecord(ev_in[c], G->io_in));
   }
   for (int c = 0; c < nch; ++c) {
-    // chunk c reads the first plane of chunk c+1 (its top neighbour)
-    VT_CUDA(cudaStreamWaitEvent(s, ev_in[c + 1 < nch ? c + 1 : c], 0));
-    VT_TRY(launch_hex8(G, H8_APPLY, false, scale, G->io_proj, G->io_raw, nullptr, G->io_v, 0.0,
-                       nullptr, nullptr, s, pb[c], pb[c + 1]));
-    VT_CUDA(cudaEventRecord(ev_k[c], s));
-    VT_CUDA(cudaStreamWaitEvent(G->io_out, ev_k[c], 0));
-    const size_t off = (size_t)(pb[c] - g.pA) * dplane;
-    VT_CUDA(cudaMemcpy2DAsync(hdst + off, row * sizeof(double), G->io_v + (size_t)pb[c] * g.nplane,
-                              (size_t)g.rp * 3 * sizeof(double), row * sizeof(double),
-                              (size_t)(pb[c + 1] - pb[c]) * (g.ny + 1), cudaMemcpyDeviceToHost,
-                              G->io_out));
+    // output planes [pb[c]-1, pb[c+1]-1): they read input planes up to pb[c+1]-1,
+    // all inside chunks <= c, so the operator on chunk c starts as soon as its
+    // own copy has landed (the last range runs to the end)
+    const int ob = c == 0 ? pb[0] : pb[c] - 1;
+    const int oe = c == nch - 1 ? pb[nch] : pb[c + 1] - 1;
+    VT_CUDA(cudaStreamWaitEvent(s, ev_in[c], 0));
+    if (oe > ob) {
+      VT_TRY(launch_hex8(G, H8_APPLY, false, scale, G->io_proj, G->io_raw, nullptr, G->io_v, 0.0,
+                         nullptr, nullptr, s, ob, oe));
+      const size_t off = (size_t)(ob - g.pA) * dplane;
+      const size_t cnt = (size_t)(oe - ob) * dplane;
+      VT_TRY(launch_pack(G, G->io_v, ob, oe, G->io_stage_out + off, s));
+      VT_CUDA(cudaEventRecord(ev_k[c], s));
+      VT_CUDA(cudaStreamWaitEvent(G->io_out, ev_k[c], 0));
+      VT_CUDA(cudaMemcpyAsync(hdst + off, G->io_stage_out + off, cnt * sizeof(double),
+                              cudaMemcpyDeviceToHost, G->io_out));
+    }
   }
   VT_CUDA(cudaEventRecord(ev_done, G->io_out));
   VT_CUDA(cudaStreamWaitEvent(s, ev_done, 0));

@@ -65,6 +65,27 @@ __global__ void unpack_project_kernel(Geom g, const uint8_t* mask, const double*
     }
   }
 }
+// vt layout planes [pa, pb) -> dense reference-order rows (contiguous D2H)
+__global__ void pack_kernel(Geom g, const double* __restrict__ src, int pa, int pb,
+                            double* __restrict__ dense) {
+  const long long w = (long long)(g.nx + 1) * 3;
+  const long long nn = (long long)(pb - pa) * (g.ny + 1) * w;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long r = t / w;
+    const long long d = t - r * w;
+    const int j = (int)(r % (g.ny + 1));
+    const int p = (int)(r / (g.ny + 1)) + pa;
+    dense[t] = src[((long long)p * (g.ny + 1) + j) * g.rp * 3 + d];
+  }
+}
+vt_status launch_pack(vt_grid* G, const double* src, int pa, int pb, double* dense, cudaStream_t s) {
+  pack_kernel<<<G->nsm * 4, VT_THREADS, 0, s>>>(G->g, src, pa, pb, dense);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 vt_status launch_unpack_project(vt_grid* G, const double* dense, int pa, int pb, double* raw,
                                 double* proj, cudaStream_t s) {
   unpack_project_kernel<<<G->nsm * 4, VT_THREADS, 0, s>>>(G->g, G->mask, dense, pa, pb, raw, proj);

@@ -85,6 +85,7 @@ struct vt_grid {
   cudaStream_t stream = nullptr;      // private stream of the blocking solver
   // streamed host-to-host apply (vt_apply_host): staging + copy streams
   double *io_stage = nullptr, *io_raw = nullptr, *io_proj = nullptr, *io_v = nullptr;
+  double* io_stage_out = nullptr;
   cudaStream_t io_in = nullptr, io_out = nullptr;
   cudaEvent_t io_ev[33] = {};
 
@@ -130,6 +131,7 @@ vt_status launch_hex8(vt_grid* G, int mode, bool dot, const double* scale, const
 vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_t s);
 vt_status launch_unpack_project(vt_grid* G, const double* dense, int pa, int pb, double* raw,
                                 double* proj, cudaStream_t s);
+vt_status launch_pack(vt_grid* G, const double* src, int pa, int pb, double* dense, cudaStream_t s);
 vt_status launch_dot(vt_grid* G, const double* x, const double* y, double* partial, int* nparts,
                      cudaStream_t s, const int* stop = nullptr);
 vt_status launch_sum_partials(const double* partial, int n, double* out, cudaStream_t s);

@@ -35,3 +35,13 @@ print("vb.apply (pinned in, new pinned out) ms", t(lambda: vb.apply(st, un)))
 print("pinned alloc ms", t(lambda: torch.empty(n, dtype=torch.float64, pin_memory=True)))
 pageable = np.array(un)
 print("vb.apply (pageable in) ms", t(lambda: vb.apply(st, pageable), k=3))
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+dv2 = torch.empty_like(dv)
+hv2 = torch.empty(n, dtype=torch.float64).pin_memory()
+def bidir():
+    with torch.cuda.stream(s1):
+        dv.copy_(hu, non_blocking=True)
+    with torch.cuda.stream(s2):
+        hv2.copy_(dv2, non_blocking=True)
+    torch.cuda.synchronize()
+print("concurrent H2D || D2H 103MB each ms", t(bidir))
