@@ -251,37 +251,58 @@ __global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double
       sc[t] = uc[node_off(gc, kk - gc.k0 + 1, jj, 0) * 3 + e];
     }
     __syncthreads();
+    // the 4 fine rows (2J+b2, 2K+c) of this unit; every dof of a row is
+    // handled together with the same dof of the other rows, so each thread
+    // has 4 independent read-modify-writes in flight
+    double* rowp[4];
+    const uint8_t* mrow[4];
+    bool ok[4];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int fk = 2 * K + c;
-      if (fk < fk0 || fk >= fk1) continue;
+    for (int q = 0; q < 4; ++q) {
+      const int c = q >> 1, b2 = q & 1;
+      const int fk = 2 * K + c, fj = 2 * J + b2;
+      ok[q] = fk >= fk0 && fk < fk1 && fj <= gf.ny;
       const int pf = fk - gf.k0 + 1;
+      rowp[q] = ok[q] ? uf + node_off(gf, pf, fj, 0) * 3 : uf;
+      mrow[q] = ok[q] ? mf + mask_off(gf, pf, fj, 0) : mf;
+    }
+    for (int d = threadIdx.x; d < fw; d += blockDim.x) {
+      const int i = d / 3, comp = d - 3 * i;
+      const int I = i >> 1;
+      double old[4];
+      unsigned mk[4];
 #pragma unroll
-      for (int b2 = 0; b2 < 2; ++b2) {
-        const int fj = 2 * J + b2;
-        if (fj > gf.ny) continue;
-        double* row = uf + node_off(gf, pf, fj, 0) * 3;
-        const uint8_t* mrow = mf + mask_off(gf, pf, fj, 0);
-        for (int d = threadIdx.x; d < fw; d += blockDim.x) {
-          const int i = d / 3, comp = d - 3 * i;
-          const int I = i >> 1;
-          auto Y = [&](int ix) {
-            double z0 = sc[(0 * 2 + 0) * cw + ix * 3 + comp];
-            double z1 = sc[(0 * 2 + 1) * cw + ix * 3 + comp];
-            if (c) {  // z pass
-              z0 = 0.5 * __dadd_rn(z0, sc[(1 * 2 + 0) * cw + ix * 3 + comp]);
-              z1 = 0.5 * __dadd_rn(z1, sc[(1 * 2 + 1) * cw + ix * 3 + comp]);
-            }
-            return b2 ? 0.5 * __dadd_rn(z0, z1) : z0;  // y pass
-          };
-          double v = Y(I);
-          if (i & 1) v = 0.5 * __dadd_rn(v, Y(I + 1));  // x pass
-          if ((mrow[i] >> comp) & 1u) v = 0.0;
-          if (ADD)
-            row[d] = __dadd_rn(row[d], v);
-          else
-            row[d] = v;
+      for (int q = 0; q < 4; ++q) {
+        old[q] = (ADD && ok[q]) ? rowp[q][d] : 0.0;
+        mk[q] = ok[q] ? mrow[q][i] : 0u;
+      }
+      // coarse corner values at x = I (and I+1): zc[kz][jy][ix]
+      double zc[2][2][2];
+#pragma unroll
+      for (int kz = 0; kz < 2; ++kz)
+#pragma unroll
+        for (int jy = 0; jy < 2; ++jy) {
+          zc[kz][jy][0] = sc[(kz * 2 + jy) * cw + I * 3 + comp];
+          zc[kz][jy][1] = (i & 1) ? sc[(kz * 2 + jy) * cw + (I + 1) * 3 + comp] : 0.0;
         }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!ok[q]) continue;
+        const int c = q >> 1, b2 = q & 1;
+        double y[2];
+#pragma unroll
+        for (int ix = 0; ix < 2; ++ix) {
+          double z0 = zc[0][0][ix], z1 = zc[0][1][ix];
+          if (c) {  // z pass
+            z0 = 0.5 * __dadd_rn(z0, zc[1][0][ix]);
+            z1 = 0.5 * __dadd_rn(z1, zc[1][1][ix]);
+          }
+          y[ix] = b2 ? 0.5 * __dadd_rn(z0, z1) : z0;  // y pass
+        }
+        double v = y[0];
+        if (i & 1) v = 0.5 * __dadd_rn(v, y[1]);  // x pass
+        if ((mk[q] >> comp) & 1u) v = 0.0;
+        rowp[q][d] = ADD ? __dadd_rn(old[q], v) : v;
       }
     }
   }

@@ -198,8 +198,10 @@ vt_status launch_diag(vt_grid* G, const double* scale, double* d, cudaStream_t s
 // One thread per node pair (i, i+1), i even: the row pitch is even, so the
 // pair's 6 doubles are 16-byte aligned and move as 3 vector loads / stores
 // (scalar per-node access was L2-request bound at 3 doubles per node).
-__global__ void jacobi0_kernel(Geom g, const uint8_t* mask, const double* scale, double kd,
-                               double omega, const double* f, double* u, const int* stop) {
+__global__ void jacobi0_kernel(Geom g, const uint8_t* __restrict__ mask,
+                               const double* __restrict__ scale, double kd, double omega,
+                               const double* __restrict__ f, double* __restrict__ u,
+                               const int* stop) {
   if (stop && *(volatile const int*)stop) return;
   const int hp = (g.nx + 2) / 2;  // node pairs per row (last may hold the pad node)
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * hp;
