@@ -63,6 +63,33 @@ static void wt_a_w(const double W[24][24], const double A[24][24], double R[24][
 }
 
 // ------------------------------------------------------------------ kernels
+// entry `entry` of the level-1 element matrix of coarse element E = (I, J, K):
+// sum_c s_c G_c + corrections (what gal_level1_kernel stores)
+struct K1Src {
+  Geom gf;
+  const double* scale;
+  const double* G;
+  const double* corr;
+  const int* corr_of;
+};
+__device__ __forceinline__ double k1_entry(const K1Src& k, long long E, int I, int J, int K, int entry) {
+  double acc = 0.0;
+  double s[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    s[c] = k.scale[elem_off(k.gf, 2 * K + (c >> 2) + 1, 2 * J + ((c >> 1) & 1), 2 * I + (c & 1))];
+    acc = fma(s[c], k.G[c * 576 + entry], acc);
+  }
+  if (k.corr_of) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int q = k.corr_of[E * 8 + c];
+      if (q >= 0) acc = __dadd_rn(acc, __dmul_rn(s[c], k.corr[(long long)q * 576 + entry]));
+    }
+  }
+  return acc;
+}
+
 // level-1 matrices from the fine scale field (vt element layout of the fine grid)
 __global__ void gal_level1_kernel(Geom gf, int cnx, int cny, int cnz, const double* __restrict__ scale,
                                   const double* __restrict__ G, const double* __restrict__ corr,
@@ -92,9 +119,12 @@ __global__ void gal_level1_kernel(Geom gf, int cnx, int cny, int cnz, const doub
 }
 
 // level l -> l+1: one CTA (192 threads, 3 entries each) per coarse element
+// (FROM_SCALE: the children are level-1 elements, formed on the fly from the
+// fine scales instead of read from storage -- level 1 stays matrix-free)
+template <bool FROM_SCALE>
 __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t* __restrict__ mask,
                                                           const double* __restrict__ mats_l,
-                                                          int cnx, int cny, int cnz,
+                                                          K1Src k1, int cnx, int cny, int cnz,
                                                           double* __restrict__ mats_c) {
   __shared__ double A[576], P[576];
   __shared__ double m[24];
@@ -113,8 +143,10 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
         m[threadIdx.x] = ((mk >> comp) & 1u) ? 0.0 : 1.0;
       }
       __syncthreads();
-      for (int q = threadIdx.x; q < 576; q += blockDim.x)
-        A[q] = mats_l[e * 576 + q] * (m[q / 24] * m[q % 24]);
+      for (int q = threadIdx.x; q < 576; q += blockDim.x) {
+        const double kq = FROM_SCALE ? k1_entry(k1, e, fi, fj, fk, q) : mats_l[e * 576 + q];
+        A[q] = kq * (m[q / 24] * m[q % 24]);
+      }
       __syncthreads();
       // P = A W_c: P[a][b] = sum_x A[a][3x + b%3] T_c[x][b/3]
       for (int q = threadIdx.x; q < 576; q += blockDim.x) {
@@ -223,9 +255,43 @@ __global__ void gal_node_kernel(Geom g, const uint8_t* __restrict__ mask, const 
   }
 }
 
+// level-1 epilogue of the matrix-free Galerkin operator (v = P^T Pi K0 Pi P x
+// already restricted, coarse fixed dofs zero): same modes as gal_node_kernel
+template <int MODE>
+__global__ void gal_vec_epilogue_kernel(Geom g, const uint8_t* __restrict__ mask,
+                                        const double* __restrict__ v, const double* __restrict__ u,
+                                        const double* __restrict__ f, const double* __restrict__ d,
+                                        double omega, double* __restrict__ out, const int* stop) {
+  if (stop && *(volatile const int*)stop) return;
+  const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (g.nx + 1));
+    const long long r = t / (g.nx + 1);
+    const int j = (int)(r % (g.ny + 1));
+    const int p = (int)(r / (g.ny + 1)) + g.pA;
+    const long long node = node_off(g, p, j, i);
+    const unsigned m = mask[mask_off(g, p, j, i)];
+#pragma unroll
+    for (int comp = 0; comp < 3; ++comp) {
+      const long long o = node * 3 + comp;
+      const bool fx = (m >> comp) & 1u;
+      double val;
+      if (MODE == 0)
+        val = fx ? u[o] : v[o];
+      else if (MODE == 1)
+        val = fx ? 0.0 : __dsub_rn(f[o], v[o]);
+      else
+        val = fx ? u[o] : __dadd_rn(u[o], __dmul_rn(omega, __ddiv_rn(__dsub_rn(f[o], v[o]), d[o])));
+      out[o] = val;
+    }
+  }
+}
+
 // per-dof diagonal: stored element diagonals summed in corner order; 1 on fixed
+template <bool FROM_SCALE>
 __global__ void gal_diag_kernel(Geom g, const uint8_t* __restrict__ mask, const double* __restrict__ mats,
-                                double* __restrict__ d) {
+                                K1Src k1, double* __restrict__ d) {
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
@@ -242,7 +308,8 @@ __global__ void gal_diag_kernel(Geom g, const uint8_t* __restrict__ mask, const 
       const long long e = ((long long)ek * g.ny + ej) * g.nx + ei;
 #pragma unroll
       for (int comp = 0; comp < 3; ++comp)
-        v[comp] = __dadd_rn(v[comp], mats[e * 576 + (3 * c + comp) * 25]);
+        v[comp] = __dadd_rn(v[comp], FROM_SCALE ? k1_entry(k1, e, ei, ej, ek, (3 * c + comp) * 25)
+                                                : mats[e * 576 + (3 * c + comp) * 25]);
     }
     const long long node = node_off(g, p, j, i);
     const unsigned m = mask[mask_off(g, p, j, i)];
@@ -344,18 +411,37 @@ vt_status gal_setup(vt_hier* H) {
   const int L = (int)H->lv.size();
   H->mats.assign(L, nullptr);
   H->gdiag.assign(L, nullptr);
+  // Level 1 is applied matrix-free as P^T (Pi K0 Pi) P through the fine kernels
+  // when it is not the coarsest level (its 576 doubles per element would be
+  // the largest array of the solver: 2.4 GB at cfg2, 65 GB at cfg5);
+  // levels >= 2 store their matrices.
+  H->gal_mf = L >= 3;
   for (int l = 1; l < L; ++l) {
     vt_grid* G2 = H->lv[l];
     const long long nel = (long long)G2->g.nx * G2->g.ny * G2->g.nz;
-    VT_CUDA(cudaMalloc(&H->mats[l], (size_t)nel * 576 * sizeof(double)));
+    if (!(l == 1 && H->gal_mf)) VT_CUDA(cudaMalloc(&H->mats[l], (size_t)nel * 576 * sizeof(double)));
     VT_CUDA(cudaMalloc(&H->gdiag[l], G2->vec_len() * sizeof(double)));
     VT_CUDA(cudaMemset(H->gdiag[l], 0, G2->vec_len() * sizeof(double)));
   }
-  VT_CUDA(cudaMalloc(&H->gve, (size_t)nel1 * 24 * sizeof(double)));
+  if (H->gal_mf) {
+    VT_CUDA(cudaMalloc(&H->gfa, F->vec_len() * sizeof(double)));
+    VT_CUDA(cudaMemset(H->gfa, 0, F->vec_len() * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->gfb, F->vec_len() * sizeof(double)));
+    VT_CUDA(cudaMemset(H->gfb, 0, F->vec_len() * sizeof(double)));
+    VT_CUDA(cudaMalloc(&H->gc1, C1->vec_len() * sizeof(double)));
+    VT_CUDA(cudaMemset(H->gc1, 0, C1->vec_len() * sizeof(double)));
+    const long long nel2 = L >= 3 ? (long long)H->lv[2]->g.nx * H->lv[2]->g.ny * H->lv[2]->g.nz : 0;
+    VT_CUDA(cudaMalloc(&H->gve, (size_t)(nel2 > 0 ? nel2 : 1) * 24 * sizeof(double)));
+  } else {
+    VT_CUDA(cudaMalloc(&H->gve, (size_t)nel1 * 24 * sizeof(double)));
+  }
   return VT_OK;
 }
 
 void gal_free(vt_hier* H) {
+  cudaFree(H->gfa);
+  cudaFree(H->gfb);
+  cudaFree(H->gc1);
   cudaFree(H->gG);
   cudaFree(H->gcorr);
   cudaFree(H->gcorr_of);
@@ -364,28 +450,48 @@ void gal_free(vt_hier* H) {
   for (double* p : H->gdiag) cudaFree(p);
 }
 
-vt_status gal_refresh(vt_hier* H, cudaStream_t s) {
-  const int L = (int)H->lv.size();
-  if (L < 2) return VT_OK;
+static K1Src k1src(vt_hier* H) {
+  return K1Src{H->lv[0]->g, H->scale[0], H->gG, H->gcorr, H->gcorr_of};
+}
+
+vt_status gal_materialize_level1(vt_hier* H, cudaStream_t s) {
   vt_grid* F = H->lv[0];
   vt_grid* C1 = H->lv[1];
   const long long tot1 = (long long)C1->g.nx * C1->g.ny * C1->g.nz * 576;
+  if (!H->mats[1]) VT_CUDA(cudaMalloc(&H->mats[1], (size_t)tot1 * sizeof(double)));
   const int grid1 = (int)std::min<long long>((tot1 + GL_THREADS - 1) / GL_THREADS, (long long)F->nsm * 16);
   gal_level1_kernel<<<grid1, GL_THREADS, 0, s>>>(F->g, C1->g.nx, C1->g.ny, C1->g.nz, H->scale[0], H->gG,
                                                  H->gcorr, H->gcorr_of, H->mats[1]);
   count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status gal_refresh(vt_hier* H, cudaStream_t s) {
+  const int L = (int)H->lv.size();
+  if (L < 2) return VT_OK;
+  const K1Src k1 = k1src(H);
+  if (!H->gal_mf) VT_TRY(gal_materialize_level1(H, s));
+  H->mats1_fresh = !H->gal_mf;
   for (int l = 1; l + 1 < L; ++l) {
     vt_grid* Gl = H->lv[l];
     vt_grid* Gc = H->lv[l + 1];
     const long long nelc = (long long)Gc->g.nx * Gc->g.ny * Gc->g.nz;
     const int grid = (int)std::min<long long>(nelc, (long long)Gl->nsm * 32);
-    gal_coarsen_kernel<<<grid, 192, 0, s>>>(Gl->g, Gl->mask, H->mats[l], Gc->g.nx, Gc->g.ny, Gc->g.nz,
-                                            H->mats[l + 1]);
+    if (l == 1 && H->gal_mf)
+      gal_coarsen_kernel<true><<<grid, 192, 0, s>>>(Gl->g, Gl->mask, nullptr, k1, Gc->g.nx, Gc->g.ny,
+                                                    Gc->g.nz, H->mats[l + 1]);
+    else
+      gal_coarsen_kernel<false><<<grid, 192, 0, s>>>(Gl->g, Gl->mask, H->mats[l], k1, Gc->g.nx, Gc->g.ny,
+                                                     Gc->g.nz, H->mats[l + 1]);
     count_launch();
   }
   for (int l = 1; l < L; ++l) {
     vt_grid* Gl = H->lv[l];
-    gal_diag_kernel<<<Gl->nsm * 4, GL_THREADS, 0, s>>>(Gl->g, Gl->mask, H->mats[l], H->gdiag[l]);
+    if (l == 1 && H->gal_mf)
+      gal_diag_kernel<true><<<Gl->nsm * 4, GL_THREADS, 0, s>>>(Gl->g, Gl->mask, nullptr, k1, H->gdiag[l]);
+    else
+      gal_diag_kernel<false><<<Gl->nsm * 4, GL_THREADS, 0, s>>>(Gl->g, Gl->mask, H->mats[l], k1, H->gdiag[l]);
     count_launch();
   }
   VT_CUDA(cudaGetLastError());
@@ -396,6 +502,29 @@ vt_status gal_refresh(vt_hier* H, cudaStream_t s) {
 vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const double* f, double* out,
                        const int* stop, cudaStream_t s) {
   vt_grid* G = H->lv[l];
+  if (l == 1 && H->gal_mf) {
+    // K1 x = Pi1 P^T Pi0 K0 Pi0 P Pi1 x through the fine-level kernels
+    vt_grid* F = H->lv[0];
+    const double* x = u;
+    if (mode == 0) {  // API apply: the input may be non-zero on fixed dofs
+      VT_TRY(launch_project(G, u, G->scratch, s));
+      x = G->scratch;
+    }
+    VT_TRY(launch_prolong_set(G, F, x, H->gfa, stop, s));
+    VT_TRY(launch_hex8(F, H8_APPLY, false, H->scale[0], H->gfa, nullptr, nullptr, H->gfb, 0.0,
+                       nullptr, stop, s));
+    VT_TRY(launch_restrict(F, G, H->gfb, H->gc1, stop, -1, -1, s));
+    const int grid_n = G->nsm * 4;
+    if (mode == 0)
+      gal_vec_epilogue_kernel<0><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
+    else if (mode == 1)
+      gal_vec_epilogue_kernel<1><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
+    else
+      gal_vec_epilogue_kernel<2><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
+    count_launch();
+    VT_CUDA(cudaGetLastError());
+    return VT_OK;
+  }
   const long long nel = (long long)G->g.nx * G->g.ny * G->g.nz;
   const int grid_e = (int)std::min<long long>((nel * 32 + GL_THREADS - 1) / GL_THREADS, (long long)G->nsm * 16);
   gal_elem_kernel<<<grid_e, GL_THREADS, 0, s>>>(G->g, G->mask, H->mats[l], u, H->gve, stop);

@@ -318,6 +318,14 @@ vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* u
   return VT_OK;
 }
 
+vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
+                             cudaStream_t s) {
+  prolong_kernel<false><<<F->nsm * 8, MG_THREADS, prolong_smem(C->g), s>>>(C->g, F->g, F->mask, uc, uf, stop);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 vt_status launch_coarsen_mask(vt_grid* F, vt_grid* C, cudaStream_t s) {
   coarsen_mask_kernel<<<C->nsm * 4, MG_THREADS, 0, s>>>(F->g, C->g, F->mask, C->mask);
   count_launch();
@@ -679,7 +687,12 @@ vt_grid* vt_hier_grid(vt_hier* H, int l) {
 }
 const double* vt_hier_level_scale(vt_hier* H, int l) { return H->scale[l]; }
 const double* vt_hier_level_mats(vt_hier* H, int l) {
-  return (H && H->scheme == 1 && l >= 1 && l < (int)H->lv.size()) ? H->mats[l] : nullptr;
+  if (!H || H->scheme != 1 || l < 1 || l >= (int)H->lv.size()) return nullptr;
+  if (l == 1 && H->gal_mf && !H->mats1_fresh) {  // matrix-free level 1: materialize on demand
+    if (gal_materialize_level1(H, 0) != VT_OK || cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    H->mats1_fresh = true;
+  }
+  return H->mats[l];
 }
 int vt_hier_scheme(const vt_hier* H) { return H ? H->scheme : -1; }
 const double* vt_hier_level_rho(vt_hier* H, int l) { return H->rho[l]; }

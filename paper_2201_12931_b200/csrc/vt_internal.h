@@ -112,6 +112,9 @@ struct vt_hier {
   double *gG = nullptr, *gcorr = nullptr, *gve = nullptr;
   int* gcorr_of = nullptr;
   std::vector<double*> mats, gdiag;  // per level (index >= 1)
+  bool gal_mf = false;              // level 1 applied matrix-free (P^T K0 P)
+  bool mats1_fresh = false;         // mats[1] materialized for the current refresh
+  double *gfa = nullptr, *gfb = nullptr, *gc1 = nullptr;  // fine x2 / level-1 scratch
 };
 
 namespace vt {
@@ -158,4 +161,7 @@ vt_status gal_refresh(vt_hier* H, cudaStream_t s);
 vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const double* f, double* out,
                        const int* stop, cudaStream_t s);
 vt_status gal_jacobi0(vt_hier* H, int l, const double* f, double* u, const int* stop, cudaStream_t s);
+vt_status gal_materialize_level1(vt_hier* H, cudaStream_t s);
+vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
+                             cudaStream_t s);
 }  // namespace vt
