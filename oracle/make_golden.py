@@ -163,6 +163,20 @@ def gen_galerkin(vt):
     np.savez_compressed(os.path.join(OUT, "galerkin.npz"), **out)
 
 
+def gen_io(vt):
+    """TPF1 checkpoint and VTI files written by the reference (app/io.py)."""
+    from voxtop.app import io as rio
+
+    rng = np.random.default_rng(5)
+    grid = vt.build_grid(4, 3, 2, 0.75)
+    rho = rng.uniform(0.0, 1.0, grid.n_elements)
+    u = rng.standard_normal(grid.n_dofs)
+    np.savez_compressed(os.path.join(OUT, "io.npz"), rho=rho, u=u, dims=np.array([4, 3, 2]), h=0.75, it=7)
+    rio.checkpoint_save(os.path.join(OUT, "io_ckpt.bin"), grid, 7, rho, u)
+    rio.export_vti(rho, grid, os.path.join(OUT, "io_bin.vti"), binary=True)
+    rio.export_vti(rho, grid, os.path.join(OUT, "io_ascii.vti"), binary=False)
+
+
 def gen_pcg(vt):
     from voxtop.app.presets import instantiate
     from voxtop.solver import jacobi_preconditioner
@@ -357,13 +371,13 @@ def gen_traj(vt, which):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="k0,operator,multigrid,galerkin,pcg,design,small,bridge,grav,cfg1,galtraj")
+    ap.add_argument("--only", default="k0,operator,multigrid,galerkin,io,pcg,design,small,bridge,grav,cfg1,galtraj")
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     vt = _vt()
     which = set(a.only.split(","))
     for name, fn in (("k0", gen_k0), ("operator", gen_operator), ("multigrid", gen_multigrid),
-                     ("galerkin", gen_galerkin), ("pcg", gen_pcg), ("design", gen_design)):
+                     ("galerkin", gen_galerkin), ("io", gen_io), ("pcg", gen_pcg), ("design", gen_design)):
         if name in which:
             t = time.perf_counter()
             fn(vt)
