@@ -261,6 +261,11 @@ vt_status vt_dist_pcg(vt_dist *D, const double *const *f, double *const *x, int 
 vt_status vt_dist_sensitivities(vt_dist *D, double *const *u, const double *const *rho, double p,
                                 double kmin, double E, int grav_axis, double grav_coef,
                                 double *const *dc, void *stream);
+/* self-weight load f = scatter(rho_e g_unit) (+ f_ext), zero on fixed if
+ * zero_fixed [ref: optimize.py:216-231]; exchanges the element layer below */
+vt_status vt_dist_gravity_load(vt_dist *D, const double *const *rho, int grav_axis, double grav_coef,
+                               const double *const *f_ext, int zero_fixed, double *const *f,
+                               void *stream);
 vt_status vt_dist_filter_create(vt_dist *D, int R, const double *kernel_host);
 vt_status vt_dist_filter_apply(vt_dist *D, const double *const *dc, const double *const *rho,
                                double gamma, double *const *dcf, void *stream);

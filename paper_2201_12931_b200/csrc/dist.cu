@@ -518,6 +518,7 @@ vt_status vt_dist_destroy(vt_dist* D) {
   cudaFree(D->fw); cudaFree(D->opart);
   for (double* p : D->fwsum) cudaFree(p);
   for (double* p : D->fprod) cudaFree(p);
+  for (double* p : D->gpad) cudaFree(p);
   if (D->comm) nccl().CommDestroy(D->comm);
   delete D;
   return VT_OK;

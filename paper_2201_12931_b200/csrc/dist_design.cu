@@ -126,6 +126,40 @@ __global__ void part_max_kernel(const double* part, int n, double* out) {
 
 static int doc_grid(vt_grid* G) { return G->nsm * 2; }
 
+// self-weight load on a slab: f = sum over incident elements (corner order) of
+// rho_e g_unit (+ f_ext), fixed -> 0 [ref: optimize.py:216-231]; rho_pad holds
+// element layers k0-1 .. k1-1 (the first one from the rank below)
+__global__ void dgrav_kernel(Geom g, const uint8_t* __restrict__ mask, const double* __restrict__ rho_pad,
+                             int gax, double gcoef, const double* __restrict__ fext, int zero_fixed,
+                             double* __restrict__ f) {
+  const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (g.nx + 1));
+    const long long r = t / (g.nx + 1);
+    const int j = (int)(r % (g.ny + 1));
+    const int p = (int)(r / (g.ny + 1)) + g.pA;
+    const int k = p - 1 + g.k0;
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int ei = i - (c & 1), ej = j - ((c >> 1) & 1), ek = k - ((c >> 2) & 1);
+      if (ei < 0 || ei >= g.nx || ej < 0 || ej >= g.ny || ek < 0 || ek < g.k0 - 1 || ek >= g.k1) continue;
+      const long long e = ((long long)(ek - g.k0 + 1) * g.ny + ej) * g.nx + ei;
+      acc = __dadd_rn(acc, __dmul_rn(rho_pad[e], gcoef));
+    }
+    const long long node = node_off(g, p, j, i);
+    const unsigned m = mask[mask_off(g, p, j, i)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double v = (c == gax) ? acc : 0.0;
+      if (fext) v = __dadd_rn(v, fext[node * 3 + c]);
+      if (zero_fixed && ((m >> c) & 1u)) v = 0.0;
+      f[node * 3 + c] = v;
+    }
+  }
+}
+
 // R ghost element layers of prod on both sides (plain layout, layer = nx*ny)
 static vt_status halo_prod(vt_dist* D, cudaStream_t s) {
   if (D->N == 1 || D->fR == 0) return VT_OK;
@@ -210,6 +244,52 @@ vt_status vt_dist_sensitivities(vt_dist* D, double* const* u, const double* cons
   for (int i = 0; i < D->nlocal; ++i)
     VT_TRY(vt_sensitivities(D->sl[i].lv[0], u[i], rho[i], p, kmin, E, grav_axis, grav_coef, dc[i],
                             stream));
+  return VT_OK;
+}
+
+// f = gravity load of rho (+ f_ext), zero on fixed dofs when zero_fixed
+vt_status vt_dist_gravity_load(vt_dist* D, const double* const* rho, int grav_axis, double grav_coef,
+                               const double* const* f_ext, int zero_fixed, double* const* f,
+                               void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long layer = (long long)D->nx * D->ny;
+  if (D->gpad.empty()) {
+    D->gpad.assign(D->nlocal, nullptr);
+    for (int i = 0; i < D->nlocal; ++i) {
+      vt_grid* G = D->sl[i].lv[0];
+      const size_t n = (size_t)(G->g.k1 - G->g.k0 + 1) * layer;
+      VT_CUDA(cudaMalloc(&D->gpad[i], n * sizeof(double)));
+      VT_CUDA(cudaMemset(D->gpad[i], 0, n * sizeof(double)));
+    }
+  }
+  for (int i = 0; i < D->nlocal; ++i) {
+    vt_grid* G = D->sl[i].lv[0];
+    VT_CUDA(cudaMemcpyAsync(D->gpad[i] + layer, rho[i], G->nel_local() * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  if (D->N > 1) {  // layer k0-1 from the rank below
+    auto nl = [&](int i) { const Geom& g = D->sl[i].lv[0]->g; return g.k1 - g.k0; };
+    if (!D->remote()) {
+      for (int i = 1; i < D->N; ++i)
+        VT_CUDA(cudaMemcpyAsync(D->gpad[i], D->gpad[i - 1] + (size_t)nl(i - 1) * layer,
+                                layer * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else {
+      const int r = D->sl[0].rank;
+      auto& A = nccl();
+      VT_NCCL(A.GroupStart());
+      if (r < D->N - 1)
+        VT_NCCL(A.Send(D->gpad[0] + (size_t)nl(0) * layer, layer, ncclDouble, r + 1, D->comm, s));
+      if (r > 0) VT_NCCL(A.Recv(D->gpad[0], layer, ncclDouble, r - 1, D->comm, s));
+      VT_NCCL(A.GroupEnd());
+    }
+  }
+  for (int i = 0; i < D->nlocal; ++i) {
+    vt_grid* G = D->sl[i].lv[0];
+    dgrav_kernel<<<G->nsm * 8, DD_THREADS, 0, s>>>(G->g, G->mask, D->gpad[i], grav_axis, grav_coef,
+                                                   f_ext ? f_ext[i] : nullptr, zero_fixed, f[i]);
+    count_launch();
+  }
+  VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 

@@ -67,6 +67,7 @@ struct vt_dist {
   double* fw = nullptr;                 // (2R+1)^3 kernel
   std::vector<double*> fwsum, fprod;    // per slab: correlate(1), rho*dc with R ghost layers
   double* opart = nullptr;              // OC / change partials (per slab, 4096 x 4)
+  std::vector<double*> gpad;            // per slab: rho with the element layer below (gravity)
 
   bool remote() const { return comm != nullptr; }
 };

@@ -261,8 +261,6 @@ class SlabRun:
                  init_densities=None, group=None):
         from .design import filter_weights, initial_densities
 
-        if problem.boundary.gravity is not None:
-            raise NotImplementedError("self-weight loads are not distributed yet; use run()")
         if solver.preconditioner != "multigrid":
             raise ValueError("the slab solver implements the multigrid preconditioner")
         grid = problem.grid
@@ -272,7 +270,9 @@ class SlabRun:
                                 nccl_id=nccl_id, nu=problem.nu)
         f_ext = problem.boundary.external_force(grid)
         f_ext[fm] = 0.0
-        self.f = S.upload(f_ext)
+        self.f_ext = S.upload(f_ext)
+        self.gravity = problem.boundary.gravity
+        self.f = S.zeros() if self.gravity is not None else self.f_ext
         rho0 = (init_densities.values if init_densities is not None
                 else initial_densities(problem.regions, opt.volfrac).values)
         self.rho = S._slab_rho(rho0)
@@ -313,15 +313,25 @@ class SlabRun:
                                             stream_ptr()))
         check(lib.vt_dist_refresh(S._h, _ptr_array(self.rho), _ptr_array(S.scales), model.p,
                                   model.kmin_frac, model.E, stream_ptr()), "vt_dist_refresh")
+        if self.gravity is not None:  # design-dependent load (optimize.py:216-231, 397-400)
+            check(lib.vt_dist_gravity_load(S._h, _ptr_array(self.rho), int(self.gravity.axis), self._gco(),
+                                           _ptr_array(self.f_ext), 1, _ptr_array(self.f), stream_ptr()))
         self.u, rep = S.mgcg_solve(self.f, u_prev=self.u, cfg=self.solver)
         return rep
+
+    def _gco(self) -> float:
+        from .material import gravity_coefficient
+
+        g = self.gravity
+        return gravity_coefficient(g.g, self.problem.grid.h, g.unit_weight)
 
     def design_step(self, model):
         """compliance, sensitivities, filter, OC; swaps rho. Returns (c, change, volume)."""
         S, opt = self.S, self.opt
         c = S.dot(self.f, self.u)
+        gax, gco = (int(self.gravity.axis), self._gco()) if self.gravity is not None else (-1, 0.0)
         check(lib.vt_dist_sensitivities(S._h, _ptr_array(self.u), _ptr_array(self.rho), model.p,
-                                        model.kmin_frac, model.E, -1, 0.0, _ptr_array(self.dc), stream_ptr()))
+                                        model.kmin_frac, model.E, gax, gco, _ptr_array(self.dc), stream_ptr()))
         check(lib.vt_dist_filter_apply(S._h, _ptr_array(self.dc), _ptr_array(self.rho), float(opt.gamma),
                                        _ptr_array(self.dcf), stream_ptr()))
         lam, steps = C.c_double(), C.c_int()

@@ -163,3 +163,19 @@ def test_slab_filter_bit_identical():
                                         stream_ptr()) == 0
         got = torch.cat(out).cpu().numpy()
         assert np.array_equal(got, ref), radius
+
+
+def test_slab_design_loop_with_self_weight():
+    """Design-dependent (self-weight) load on slabs: the load lumping reads the
+    element layer below each slab (exchanged), sensitivities carry 2 u.g."""
+    from paper_2201_12931_b200 import cases
+    from paper_2201_12931_b200.slabs import run_slabs
+
+    prob = cases.selfweight(32, 16, 16, 1e-3)
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * prob.grid.h, max_iterations=4, ch_tol=1e-12)
+    cfg = vb.SolverConfig(tolerance=1e-10, max_iterations=1000)
+    ref = vb.run(prob, opt, cfg, scheme="homogenized", max_levels=4)
+    got = run_slabs(prob, opt, cfg, max_levels=4, nranks=4)
+    for a, b in zip(got.records, ref.records):
+        assert abs(a.compliance - b.compliance) <= 1e-9 * abs(b.compliance), (a, b)
+    assert np.abs(got.densities.values - ref.densities.values).max() <= 1e-8
