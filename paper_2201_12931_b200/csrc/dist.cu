@@ -78,6 +78,7 @@ NcclApi& nccl() {
 // true residual from the hex8 grid, else the recurrence from the dot grid)
 __global__ void slab_sum_kernel(const PcgCtl* ctl, const double* partial, int n, int n50,
                                 double* out) {
+  griddep_wait();
   if (ctl && ctl->stop) return;
   const int cnt = (ctl && n50 > 0 && (ctl->k % 50) == 0) ? n50 : n;
   const double s = warp_sum_partials(partial, cnt);
@@ -162,7 +163,7 @@ vt_status gather_scal(vt_dist* D, int slot, cudaStream_t s) {
 
 vt_status slab_sum(vt_dist* D, int i, const double* partial, int n, int n50, int slot,
                           const PcgCtl* ctl, cudaStream_t s) {
-  slab_sum_kernel<<<1, 32, 0, s>>>(ctl, partial, n, n50,
+  launch_pdl(slab_sum_kernel, 1, 32, 0, s, ctl, partial, n, n50,
                                    D->scal + (size_t)slot * D->N + D->sl[i].rank);
   count_launch();
   VT_CUDA(cudaGetLastError());

@@ -94,6 +94,7 @@ __device__ __forceinline__ double k1_entry(const K1Src& k, long long E, int I, i
 __global__ void gal_level1_kernel(Geom gf, int cnx, int cny, int cnz, const double* __restrict__ scale,
                                   const double* __restrict__ G, const double* __restrict__ corr,
                                   const int* __restrict__ corr_of, double* __restrict__ mats) {
+  griddep_wait();
   const long long total = (long long)cnx * cny * cnz * 576;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
                                                           const double* __restrict__ mats_l,
                                                           K1Src k1, int cnx, int cny, int cnz,
                                                           double* __restrict__ mats_c) {
+  griddep_wait();
   __shared__ double A[576], P[576];
   __shared__ double m[24];
   const long long nelc = (long long)cnx * cny * cnz;
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
 __global__ void gal_elem_kernel(Geom g, const uint8_t* __restrict__ mask,
                                 const double* __restrict__ mats, const double* __restrict__ u,
                                 double* __restrict__ ve, const int* stop) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   __shared__ double us[8][24];
   const long long nel = (long long)g.nx * g.ny * g.nz;
@@ -218,6 +221,7 @@ __global__ void gal_node_kernel(Geom g, const uint8_t* __restrict__ mask, const 
                                 const double* __restrict__ u, const double* __restrict__ f,
                                 const double* __restrict__ d, double omega, double* __restrict__ out,
                                 const int* stop) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
@@ -262,6 +266,7 @@ __global__ void gal_vec_epilogue_kernel(Geom g, const uint8_t* __restrict__ mask
                                         const double* __restrict__ v, const double* __restrict__ u,
                                         const double* __restrict__ f, const double* __restrict__ d,
                                         double omega, double* __restrict__ out, const int* stop) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
@@ -292,6 +297,7 @@ __global__ void gal_vec_epilogue_kernel(Geom g, const uint8_t* __restrict__ mask
 template <bool FROM_SCALE>
 __global__ void gal_diag_kernel(Geom g, const uint8_t* __restrict__ mask, const double* __restrict__ mats,
                                 K1Src k1, double* __restrict__ d) {
+  griddep_wait();
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
@@ -322,6 +328,7 @@ __global__ void gal_diag_kernel(Geom g, const uint8_t* __restrict__ mask, const 
 __global__ void gal_jacobi0_kernel(Geom g, const uint8_t* __restrict__ mask, const double* __restrict__ f,
                                    const double* __restrict__ d, double omega, double* __restrict__ u,
                                    const int* stop) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
@@ -460,7 +467,7 @@ vt_status gal_materialize_level1(vt_hier* H, cudaStream_t s) {
   const long long tot1 = (long long)C1->g.nx * C1->g.ny * C1->g.nz * 576;
   if (!H->mats[1]) VT_CUDA(cudaMalloc(&H->mats[1], (size_t)tot1 * sizeof(double)));
   const int grid1 = (int)std::min<long long>((tot1 + GL_THREADS - 1) / GL_THREADS, (long long)F->nsm * 16);
-  gal_level1_kernel<<<grid1, GL_THREADS, 0, s>>>(F->g, C1->g.nx, C1->g.ny, C1->g.nz, H->scale[0], H->gG,
+  launch_pdl(gal_level1_kernel, grid1, GL_THREADS, 0, s, F->g, C1->g.nx, C1->g.ny, C1->g.nz, H->scale[0], H->gG,
                                                  H->gcorr, H->gcorr_of, H->mats[1]);
   count_launch();
   VT_CUDA(cudaGetLastError());
@@ -479,19 +486,19 @@ vt_status gal_refresh(vt_hier* H, cudaStream_t s) {
     const long long nelc = (long long)Gc->g.nx * Gc->g.ny * Gc->g.nz;
     const int grid = (int)std::min<long long>(nelc, (long long)Gl->nsm * 32);
     if (l == 1 && H->gal_mf)
-      gal_coarsen_kernel<true><<<grid, 192, 0, s>>>(Gl->g, Gl->mask, nullptr, k1, Gc->g.nx, Gc->g.ny,
+      launch_pdl(gal_coarsen_kernel<true>, grid, 192, 0, s, Gl->g, Gl->mask, nullptr, k1, Gc->g.nx, Gc->g.ny,
                                                     Gc->g.nz, H->mats[l + 1]);
     else
-      gal_coarsen_kernel<false><<<grid, 192, 0, s>>>(Gl->g, Gl->mask, H->mats[l], k1, Gc->g.nx, Gc->g.ny,
+      launch_pdl(gal_coarsen_kernel<false>, grid, 192, 0, s, Gl->g, Gl->mask, H->mats[l], k1, Gc->g.nx, Gc->g.ny,
                                                      Gc->g.nz, H->mats[l + 1]);
     count_launch();
   }
   for (int l = 1; l < L; ++l) {
     vt_grid* Gl = H->lv[l];
     if (l == 1 && H->gal_mf)
-      gal_diag_kernel<true><<<Gl->nsm * 4, GL_THREADS, 0, s>>>(Gl->g, Gl->mask, nullptr, k1, H->gdiag[l]);
+      launch_pdl(gal_diag_kernel<true>, Gl->nsm * 4, GL_THREADS, 0, s, Gl->g, Gl->mask, nullptr, k1, H->gdiag[l]);
     else
-      gal_diag_kernel<false><<<Gl->nsm * 4, GL_THREADS, 0, s>>>(Gl->g, Gl->mask, H->mats[l], k1, H->gdiag[l]);
+      launch_pdl(gal_diag_kernel<false>, Gl->nsm * 4, GL_THREADS, 0, s, Gl->g, Gl->mask, H->mats[l], k1, H->gdiag[l]);
     count_launch();
   }
   VT_CUDA(cudaGetLastError());
@@ -516,25 +523,25 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
     VT_TRY(launch_restrict(F, G, H->gfb, H->gc1, stop, -1, -1, s));
     const int grid_n = G->nsm * 4;
     if (mode == 0)
-      gal_vec_epilogue_kernel<0><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
+      launch_pdl(gal_vec_epilogue_kernel<0>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
     else if (mode == 1)
-      gal_vec_epilogue_kernel<1><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
+      launch_pdl(gal_vec_epilogue_kernel<1>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
     else
-      gal_vec_epilogue_kernel<2><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
+      launch_pdl(gal_vec_epilogue_kernel<2>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
     count_launch();
     VT_CUDA(cudaGetLastError());
     return VT_OK;
   }
   const long long nel = (long long)G->g.nx * G->g.ny * G->g.nz;
   const int grid_e = (int)std::min<long long>((nel * 32 + GL_THREADS - 1) / GL_THREADS, (long long)G->nsm * 16);
-  gal_elem_kernel<<<grid_e, GL_THREADS, 0, s>>>(G->g, G->mask, H->mats[l], u, H->gve, stop);
+  launch_pdl(gal_elem_kernel, grid_e, GL_THREADS, 0, s, G->g, G->mask, H->mats[l], u, H->gve, stop);
   const int grid_n = G->nsm * 4;
   if (mode == 0)
-    gal_node_kernel<0><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gve, u, f, H->gdiag[l], H->omega, out, stop);
+    launch_pdl(gal_node_kernel<0>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gve, u, f, H->gdiag[l], H->omega, out, stop);
   else if (mode == 1)
-    gal_node_kernel<1><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gve, u, f, H->gdiag[l], H->omega, out, stop);
+    launch_pdl(gal_node_kernel<1>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gve, u, f, H->gdiag[l], H->omega, out, stop);
   else
-    gal_node_kernel<2><<<grid_n, GL_THREADS, 0, s>>>(G->g, G->mask, H->gve, u, f, H->gdiag[l], H->omega, out, stop);
+    launch_pdl(gal_node_kernel<2>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gve, u, f, H->gdiag[l], H->omega, out, stop);
   count_launch(2);
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -542,7 +549,7 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
 
 vt_status gal_jacobi0(vt_hier* H, int l, const double* f, double* u, const int* stop, cudaStream_t s) {
   vt_grid* G = H->lv[l];
-  gal_jacobi0_kernel<<<G->nsm * 4, GL_THREADS, 0, s>>>(G->g, G->mask, f, H->gdiag[l], H->omega, u, stop);
+  launch_pdl(gal_jacobi0_kernel, G->nsm * 4, GL_THREADS, 0, s, G->g, G->mask, f, H->gdiag[l], H->omega, u, stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;

@@ -46,6 +46,7 @@ __device__ __forceinline__ double simp_pow(double r, double p) {
 
 __global__ void scale_kernel(Geom g, const double* rho, double p, double kmin, double E,
                              double* scale, int* bad) {
+  griddep_wait();
   const long long nel = (long long)g.nx * g.ny * (g.k1 - g.k0);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
        e += (long long)gridDim.x * blockDim.x) {
@@ -63,7 +64,7 @@ __global__ void scale_kernel(Geom g, const double* rho, double p, double kmin, d
 
 vt_status launch_scale(vt_grid* G, const double* rho, double p, double kmin, double E,
                        double* scale, int* bad, cudaStream_t s) {
-  scale_kernel<<<G->nsm * 8, MG_THREADS, 0, s>>>(G->g, rho, p, kmin, E, scale, bad);
+  launch_pdl(scale_kernel, G->nsm * 8, MG_THREADS, 0, s, G->g, rho, p, kmin, E, scale, bad);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -73,6 +74,7 @@ vt_status launch_scale(vt_grid* G, const double* rho, double p, double kmin, dou
 // rho_c = mean of the 8 children, numpy pairwise order
 __global__ void coarsen_rho_kernel(int fnx, int fny, int cnx, int cny, int cnz,
                                    const double* __restrict__ rf, double* __restrict__ rc) {
+  griddep_wait();
   const long long nel = (long long)cnx * cny * cnz;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
        e += (long long)gridDim.x * blockDim.x) {
@@ -94,6 +96,7 @@ __global__ void coarsen_rho_kernel(int fnx, int fny, int cnx, int cny, int cnz,
 
 // coarse dof fixed <=> coincident fine dof fixed [ref: multigrid.py:137-141]
 __global__ void coarsen_mask_kernel(Geom gf, Geom gc, const uint8_t* mf, uint8_t* mc) {
+  griddep_wait();
   const long long nn = owned_nodes(gc);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
@@ -106,6 +109,7 @@ __global__ void coarsen_mask_kernel(Geom gf, Geom gc, const uint8_t* mf, uint8_t
 }
 
 __global__ void count_fixed_kernel(Geom g, const uint8_t* m, unsigned long long* out) {
+  griddep_wait();
   const long long nn = owned_nodes(g);
   unsigned long long c = 0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
@@ -128,6 +132,7 @@ __global__ void count_fixed_kernel(Geom g, const uint8_t* m, unsigned long long*
 // and combines them in the reference's pass order (bit-identical).
 __global__ void restrict_kernel(Geom gf, Geom gc, const uint8_t* mc, const double* __restrict__ rf,
                                 double* __restrict__ fc, const int* stop, int kb, int ke) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   const long long nn = (long long)(ke - kb) * (gc.ny + 1) * (gc.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
@@ -215,7 +220,7 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
     ke = C->g.k1 + C->g.last;
   }
   if (ke <= kb) return VT_OK;
-  restrict_kernel<<<C->nsm * 4, MG_THREADS, 0, s>>>(F->g, C->g, C->mask, rf, fc, stop, kb, ke);
+  launch_pdl(restrict_kernel, C->nsm * 4, MG_THREADS, 0, s, F->g, C->g, C->mask, rf, fc, stop, kb, ke);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -233,6 +238,7 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
 template <bool ADD>
 __global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double* __restrict__ uc,
                                double* __restrict__ uf, const int* stop) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   extern __shared__ double sc[];                        // [kz][jy][cw]
   const int fk0 = gf.k0 + gf.pA - 1;                    // first owned fine plane
@@ -312,7 +318,7 @@ static size_t prolong_smem(const Geom& gc) { return (size_t)4 * (gc.nx + 1) * 3 
 
 vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
                              const int* stop, cudaStream_t s) {
-  prolong_kernel<true><<<F->nsm * 8, MG_THREADS, prolong_smem(C->g), s>>>(C->g, F->g, F->mask, uc, uf, stop);
+  launch_pdl(prolong_kernel<true>, F->nsm * 8, MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -320,21 +326,21 @@ vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* u
 
 vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
                              cudaStream_t s) {
-  prolong_kernel<false><<<F->nsm * 8, MG_THREADS, prolong_smem(C->g), s>>>(C->g, F->g, F->mask, uc, uf, stop);
+  launch_pdl(prolong_kernel<false>, F->nsm * 8, MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 
 vt_status launch_coarsen_mask(vt_grid* F, vt_grid* C, cudaStream_t s) {
-  coarsen_mask_kernel<<<C->nsm * 4, MG_THREADS, 0, s>>>(F->g, C->g, F->mask, C->mask);
+  launch_pdl(coarsen_mask_kernel, C->nsm * 4, MG_THREADS, 0, s, F->g, C->g, F->mask, C->mask);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 
 vt_status launch_coarsen_rho(vt_grid* F, vt_grid* C, const double* rf, double* rc, cudaStream_t s) {
-  coarsen_rho_kernel<<<C->nsm * 4, MG_THREADS, 0, s>>>(F->g.nx, F->g.ny, C->g.nx, C->g.ny,
+  launch_pdl(coarsen_rho_kernel, C->nsm * 4, MG_THREADS, 0, s, F->g.nx, F->g.ny, C->g.nx, C->g.ny,
                                                       C->g.k1 - C->g.k0, rf, rc);
   count_launch();
   VT_CUDA(cudaGetLastError());
@@ -347,6 +353,7 @@ vt_status launch_coarsen_rho(vt_grid* F, vt_grid* C, const double* rf, double* r
 __global__ void __launch_bounds__(1024, 1)
     coarse_factor_kernel(Geom g, const double* scale, const double* k0l, const double* mats,
                          const uint8_t* mask, int n, double* A, double* A0, int* status) {
+  griddep_wait();
   const int nx1 = g.nx + 1, ny1 = g.ny + 1;
   for (long long t = threadIdx.x; t < (long long)n * n; t += blockDim.x) A[t] = 0.0;
   __syncthreads();
@@ -414,6 +421,7 @@ __global__ void __launch_bounds__(1024, 1)
 
 // W = L^{-1}: one thread per column
 __global__ void tri_inverse_kernel(int n, const double* A, double* W) {
+  griddep_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   for (int i = 0; i < c; ++i) W[(long long)i * n + c] = 0.0;
@@ -426,6 +434,7 @@ __global__ void tri_inverse_kernel(int n, const double* A, double* W) {
 
 // Kinv = W^T W
 __global__ void gram_kernel(int n, const double* W, double* Kinv) {
+  griddep_wait();
   const long long nn = (long long)n * n;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
@@ -461,6 +470,7 @@ template <int MODE>
 __global__ void coarse_mv_kernel(Geom g, const uint8_t* mask, int n, const double* M,
                                  const double* f, double* cf, double* x0, double* cr, double* u,
                                  const int* stop) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   extern __shared__ double vs[];
   for (int d = threadIdx.x; d < n; d += blockDim.x) {
@@ -519,9 +529,9 @@ vt_status launch_coarse_solve(vt_hier* H, const double* f, double* u, const int*
   const size_t sm = (size_t)n * sizeof(double);
   const int grid = (n + 7) / 8;  // one warp per row, 8 warps per CTA
   double *cf = H->cvec, *x0 = H->cvec + n, *cr = H->cvec + 2 * n;
-  coarse_mv_kernel<0><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->Kinv, f, cf, x0, cr, u, stop);
-  coarse_mv_kernel<1><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->A0, f, cf, x0, cr, u, stop);
-  coarse_mv_kernel<2><<<grid, 256, sm, s>>>(G->g, G->mask, n, H->Kinv, f, cf, x0, cr, u, stop);
+  launch_pdl(coarse_mv_kernel<0>, grid, 256, sm, s, G->g, G->mask, n, H->Kinv, f, cf, x0, cr, u, stop);
+  launch_pdl(coarse_mv_kernel<1>, grid, 256, sm, s, G->g, G->mask, n, H->A0, f, cf, x0, cr, u, stop);
+  launch_pdl(coarse_mv_kernel<2>, grid, 256, sm, s, G->g, G->mask, n, H->Kinv, f, cf, x0, cr, u, stop);
   count_launch(3);
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -579,7 +589,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
   }
   for (int l = L - 2; l >= top; --l) {
     vt_grid* G = H->lv[l];
-    prolong_kernel<true><<<G->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s>>>(H->lv[l + 1]->g, G->g, G->mask,
+    launch_pdl(prolong_kernel<true>, G->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, G->g, G->mask,
                                                            ucur[l + 1], ucur[l], stop);
     count_launch();
     VT_CUDA(cudaGetLastError());
@@ -714,7 +724,7 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
     for (int l = 1; l < L; ++l) {
       vt_grid* f = H->lv[l - 1];
       vt_grid* c = H->lv[l];
-      coarsen_rho_kernel<<<c->nsm * 4, MG_THREADS, 0, s>>>(f->g.nx, f->g.ny, c->g.nx, c->g.ny,
+      launch_pdl(coarsen_rho_kernel, c->nsm * 4, MG_THREADS, 0, s, f->g.nx, f->g.ny, c->g.nx, c->g.ny,
                                                            c->g.nz, H->rho[l - 1], H->rho[l]);
       count_launch();
       VT_TRY(launch_scale(c, H->rho[l], p, kmin, E, H->scale[l], bad, s));
@@ -751,11 +761,11 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
                                    (int)(n * sizeof(double))));
     }
   }
-  coarse_factor_kernel<<<1, 1024, 0, s>>>(C->g, H->scale[L - 1], H->k0l,
+  launch_pdl(coarse_factor_kernel, 1, 1024, 0, s, C->g, H->scale[L - 1], H->k0l,
                                           (H->scheme == 1 && L > 1) ? H->mats[L - 1] : nullptr,
                                           C->mask, n, H->A, H->A0, H->status);
-  tri_inverse_kernel<<<(n + 127) / 128, 128, 0, s>>>(n, H->A, H->W);
-  gram_kernel<<<C->nsm * 4, 256, 0, s>>>(n, H->W, H->Kinv);
+  launch_pdl(tri_inverse_kernel, (n + 127) / 128, 128, 0, s, n, H->A, H->W);
+  launch_pdl(gram_kernel, C->nsm * 4, 256, 0, s, n, H->W, H->Kinv);
   count_launch(3);
   VT_CUDA(cudaGetLastError());
   int hb[2] = {0, 0};
@@ -796,7 +806,7 @@ vt_status vt_hier_prolong(vt_hier* H, int l, const double* coarse, double* fine,
   cudaStream_t s = (cudaStream_t)stream;
   if (l < 0 || l + 1 >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
   vt_grid* F = H->lv[l];
-  prolong_kernel<false><<<F->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s>>>(H->lv[l + 1]->g, F->g, F->mask, coarse,
+  launch_pdl(prolong_kernel<false>, F->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, F->g, F->mask, coarse,
                                                           fine, nullptr);
   count_launch();
   VT_CUDA(cudaGetLastError());

@@ -8,6 +8,7 @@
 // copy of the control block one iteration behind the device.
 #include <cudaTypedefs.h>
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -22,6 +23,10 @@ namespace vt {
 
 static thread_local std::string g_err;
 unsigned long long g_launches = 0;
+bool g_pdl = [] {
+  const char* e = getenv("VT_PDL");
+  return !(e && e[0] == '0');
+}();
 
 void set_error(const std::string& msg) { g_err = msg; }
 vt_status fail(vt_status code, const std::string& msg) {

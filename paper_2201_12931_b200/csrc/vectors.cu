@@ -20,6 +20,7 @@ __device__ __forceinline__ void owned_range(const Geom& g, long long& b, long lo
 
 // ---------------------------------------------------------------- projection
 __global__ void project_kernel(Geom g, const uint8_t* mask, const double* src, double* dst) {
+  griddep_wait();
   long long b, e;
   owned_range(g, b, e);
   const long long nn = (e - b) / 3;
@@ -35,7 +36,7 @@ __global__ void project_kernel(Geom g, const uint8_t* mask, const double* src, d
 }
 
 vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_t s) {
-  project_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, G->mask, src, dst);
+  launch_pdl(project_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, G->mask, src, dst);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -47,6 +48,7 @@ vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_
 __global__ void unpack_project_kernel(Geom g, const uint8_t* mask, const double* __restrict__ dense,
                                       int pa, int pb, double* __restrict__ raw,
                                       double* __restrict__ proj) {
+  griddep_wait();
   const long long row = (long long)(g.nx + 1);
   const long long nn = (long long)(pb - pa) * (g.ny + 1) * row;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
@@ -68,6 +70,7 @@ __global__ void unpack_project_kernel(Geom g, const uint8_t* mask, const double*
 // vt layout planes [pa, pb) -> dense reference-order rows (contiguous D2H)
 __global__ void pack_kernel(Geom g, const double* __restrict__ src, int pa, int pb,
                             double* __restrict__ dense) {
+  griddep_wait();
   const long long w = (long long)(g.nx + 1) * 3;
   const long long nn = (long long)(pb - pa) * (g.ny + 1) * w;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
@@ -80,7 +83,7 @@ __global__ void pack_kernel(Geom g, const double* __restrict__ src, int pa, int 
   }
 }
 vt_status launch_pack(vt_grid* G, const double* src, int pa, int pb, double* dense, cudaStream_t s) {
-  pack_kernel<<<G->nsm * 4, VT_THREADS, 0, s>>>(G->g, src, pa, pb, dense);
+  launch_pdl(pack_kernel, G->nsm * 4, VT_THREADS, 0, s, G->g, src, pa, pb, dense);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -88,13 +91,14 @@ vt_status launch_pack(vt_grid* G, const double* src, int pa, int pb, double* den
 
 vt_status launch_unpack_project(vt_grid* G, const double* dense, int pa, int pb, double* raw,
                                 double* proj, cudaStream_t s) {
-  unpack_project_kernel<<<G->nsm * 4, VT_THREADS, 0, s>>>(G->g, G->mask, dense, pa, pb, raw, proj);
+  launch_pdl(unpack_project_kernel, G->nsm * 4, VT_THREADS, 0, s, G->g, G->mask, dense, pa, pb, raw, proj);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 
 __global__ void zero_owned_kernel(Geom g, double* v) {
+  griddep_wait();
   long long b, e;
   owned_range(g, b, e);
   for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
@@ -102,7 +106,7 @@ __global__ void zero_owned_kernel(Geom g, double* v) {
     v[i] = 0.0;
 }
 vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s) {
-  zero_owned_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, v);
+  launch_pdl(zero_owned_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, v);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -111,6 +115,7 @@ vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s) {
 // ---------------------------------------------------------------- dots
 __global__ void dot_kernel(Geom g, const double* __restrict__ x, const double* __restrict__ y,
                            double* partial, const int* stop) {
+  griddep_wait();
   __shared__ double red[VT_THREADS / 32];
   if (stop && *(volatile const int*)stop) return;
   long long b, e;
@@ -132,7 +137,7 @@ __global__ void dot_kernel(Geom g, const double* __restrict__ x, const double* _
 vt_status launch_dot(vt_grid* G, const double* x, const double* y, double* partial, int* nparts,
                      cudaStream_t s, const int* stop) {
   const int grid = dot_grid(G);
-  dot_kernel<<<grid, VT_THREADS, 0, s>>>(G->g, x, y, partial, stop);
+  launch_pdl(dot_kernel, grid, VT_THREADS, 0, s, G->g, x, y, partial, stop);
   count_launch();
   if (nparts) *nparts = grid;
   VT_CUDA(cudaGetLastError());
@@ -140,11 +145,12 @@ vt_status launch_dot(vt_grid* G, const double* x, const double* y, double* parti
 }
 
 __global__ void sum_partials_kernel(const double* p, int n, double* out) {
+  griddep_wait();
   const double s = warp_sum_partials(p, n);
   if (threadIdx.x == 0) *out = s;
 }
 vt_status launch_sum_partials(const double* partial, int n, double* out, cudaStream_t s) {
-  sum_partials_kernel<<<1, 32, 0, s>>>(partial, n, out);
+  launch_pdl(sum_partials_kernel, 1, 32, 0, s, partial, n, out);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -170,6 +176,7 @@ __device__ __forceinline__ double node_diag(const Geom& g, const double* scale, 
 
 __global__ void diag_kernel(Geom g, const uint8_t* mask, const double* scale, double kd,
                             double* out) {
+  griddep_wait();
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
        t += (long long)gridDim.x * blockDim.x) {
@@ -186,7 +193,7 @@ __global__ void diag_kernel(Geom g, const uint8_t* mask, const double* scale, do
 }
 
 vt_status launch_diag(vt_grid* G, const double* scale, double* d, cudaStream_t s) {
-  diag_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, G->mask, scale, G->coef.kd, d);
+  launch_pdl(diag_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, G->mask, scale, G->coef.kd, d);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -202,6 +209,7 @@ __global__ void jacobi0_kernel(Geom g, const uint8_t* __restrict__ mask,
                                const double* __restrict__ scale, double kd, double omega,
                                const double* __restrict__ f, double* __restrict__ u,
                                const int* stop) {
+  griddep_wait();
   if (stop && *(volatile const int*)stop) return;
   const int hp = (g.nx + 2) / 2;  // node pairs per row (last may hold the pad node)
   const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * hp;
@@ -236,7 +244,7 @@ __global__ void jacobi0_kernel(Geom g, const uint8_t* __restrict__ mask,
 
 vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const double* f,
                          double* u, const int* stop, cudaStream_t s) {
-  jacobi0_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, G->mask, scale, G->coef.kd, omega, f, u,
+  launch_pdl(jacobi0_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, G->mask, scale, G->coef.kd, omega, f, u,
                                                    stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
@@ -249,6 +257,7 @@ vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const do
 __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict__ x,
                                   const double* __restrict__ p, double* __restrict__ r,
                                   const double* __restrict__ q, double* partial, int with_r) {
+  griddep_wait();
   __shared__ double red[VT_THREADS / 32];
   // The host enqueues iteration k+1 before it sees that iteration k stopped, so
   // every pass of an iteration checks `stop` itself: S1 of a stopped solve
@@ -290,6 +299,7 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
 // p = z + beta p   [ref: solver.py:158]
 __global__ void pcg_xpby_kernel(Geom g, const PcgCtl* ctl, const double* __restrict__ z,
                                 double* __restrict__ p) {
+  griddep_wait();
   if (ctl->stop) return;
   const double beta = ctl->beta;
   long long b, e;
@@ -310,6 +320,7 @@ __global__ void pcg_xpby_kernel(Geom g, const PcgCtl* ctl, const double* __restr
 // conditional copy dst = src (skip flag)
 __global__ void copy_kernel(Geom g, const int* skip, const double* __restrict__ src,
                             double* __restrict__ dst) {
+  griddep_wait();
   if (skip && *(volatile const int*)skip) return;  // (skip_swap is 1 once stopped)
   long long b, e;
   owned_range(g, b, e);
@@ -322,6 +333,7 @@ __global__ void copy_kernel(Geom g, const int* skip, const double* __restrict__ 
 __global__ void jacobi_precond_kernel(Geom g, const int* stop, const double* __restrict__ r,
                                       const double* __restrict__ d, double* __restrict__ z,
                                       double* partial) {
+  griddep_wait();
   __shared__ double red[VT_THREADS / 32];
   if (stop && *(volatile const int*)stop) return;
   long long b, e;
@@ -343,6 +355,7 @@ __global__ void jacobi_precond_kernel(Geom g, const int* stop, const double* __r
 // ---------------------------------------------------------------- scalar steps
 // S1: pq -> alpha, iteration counter, curvature checks [ref: solver.py:121-132]
 __global__ void pcg_s1_kernel(PcgCtl* c, const double* partial, int n) {
+  griddep_wait();
   if (c->stop) return;
   const double pq = warp_sum_partials(partial, n);
   if (threadIdx.x != 0) return;
@@ -364,6 +377,7 @@ __global__ void pcg_s1_kernel(PcgCtl* c, const double* partial, int n) {
 
 // S2: rel = ||r|| / ||f|| ; candidate convergence [ref: solver.py:137-140]
 __global__ void pcg_s2_kernel(PcgCtl* c, const double* partial, int n_rec, int n_true) {
+  griddep_wait();
   if (c->stop) return;
   const int is50 = (c->k % 50) == 0;
   const double rr = warp_sum_partials(partial, is50 ? n_true : n_rec);
@@ -379,6 +393,7 @@ __global__ void pcg_s2_kernel(PcgCtl* c, const double* partial, int n_rec, int n
 
 // S3: true residual check on a convergence candidate [ref: solver.py:140-149]
 __global__ void pcg_s3_kernel(PcgCtl* c, const double* partial, int n) {
+  griddep_wait();
   if (c->skip_cand || c->stop) return;
   const double tr = warp_sum_partials(partial, n);
   if (threadIdx.x != 0) return;
@@ -396,6 +411,7 @@ __global__ void pcg_s3_kernel(PcgCtl* c, const double* partial, int n) {
 
 // S4: r.z -> beta [ref: solver.py:150-159]
 __global__ void pcg_s4_kernel(PcgCtl* c, const double* partial, int n, int counts) {
+  griddep_wait();
   if (c->stop) return;
   const double rz = warp_sum_partials(partial, n);
   if (threadIdx.x != 0) return;
@@ -410,52 +426,52 @@ __global__ void pcg_s4_kernel(PcgCtl* c, const double* partial, int n, int count
 
 vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p, double* r,
                             const double* q, double* partial, int with_r, cudaStream_t s) {
-  pcg_update_kernel<<<dot_grid(G), VT_THREADS, 0, s>>>(G->g, ctl, x, p, r, q, partial, with_r);
+  launch_pdl(pcg_update_kernel, dot_grid(G), VT_THREADS, 0, s, G->g, ctl, x, p, r, q, partial, with_r);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s) {
-  pcg_xpby_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, ctl, z, p);
+  launch_pdl(pcg_xpby_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, ctl, z, p);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 vt_status launch_copy(vt_grid* G, const int* skip, const double* src, double* dst,
                       cudaStream_t s) {
-  copy_kernel<<<G->nsm * 8, VT_THREADS, 0, s>>>(G->g, skip, src, dst);
+  launch_pdl(copy_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, skip, src, dst);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 vt_status launch_jacobi_precond(vt_grid* G, const int* stop, const double* r, const double* d,
                                 double* z, double* partial, cudaStream_t s) {
-  jacobi_precond_kernel<<<dot_grid(G), VT_THREADS, 0, s>>>(G->g, stop, r, d, z, partial);
+  launch_pdl(jacobi_precond_kernel, dot_grid(G), VT_THREADS, 0, s, G->g, stop, r, d, z, partial);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 vt_status launch_pcg_s1(PcgCtl* c, const double* partial, int n, cudaStream_t s) {
-  pcg_s1_kernel<<<1, 32, 0, s>>>(c, partial, n);
+  launch_pdl(pcg_s1_kernel, 1, 32, 0, s, c, partial, n);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 vt_status launch_pcg_s2(PcgCtl* c, const double* partial, int n_rec, int n_true,
                         cudaStream_t s) {
-  pcg_s2_kernel<<<1, 32, 0, s>>>(c, partial, n_rec, n_true);
+  launch_pdl(pcg_s2_kernel, 1, 32, 0, s, c, partial, n_rec, n_true);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 vt_status launch_pcg_s3(PcgCtl* c, const double* partial, int n, cudaStream_t s) {
-  pcg_s3_kernel<<<1, 32, 0, s>>>(c, partial, n);
+  launch_pdl(pcg_s3_kernel, 1, 32, 0, s, c, partial, n);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
 vt_status launch_pcg_s4(PcgCtl* c, const double* partial, int n, int counts, cudaStream_t s) {
-  pcg_s4_kernel<<<1, 32, 0, s>>>(c, partial, n, counts);
+  launch_pdl(pcg_s4_kernel, 1, 32, 0, s, c, partial, n, counts);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;

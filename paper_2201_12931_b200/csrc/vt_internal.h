@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -28,6 +29,23 @@ vt_status cuda_fail(cudaError_t e, const char* what);
   } while (0)
 
 extern unsigned long long g_launches;  // kernels launched by this library
+extern bool g_pdl;                     // launch with programmatic stream serialization (VT_PDL=0 off)
+
+template <typename... ExpTypes, typename... ActTypes>
+inline cudaError_t launch_pdl(void (*kernel)(ExpTypes...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, ActTypes&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<ActTypes>(args)...);
+}
 inline void count_launch(int n = 1) { g_launches += (unsigned long long)n; }
 
 // Element-operator constants of one level (factorized hex8):
