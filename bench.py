@@ -247,6 +247,10 @@ def run_ours(a):
     if a.simp_iters > 0 and not slabs:
         opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
         R = DeviceRun(problem, opt, vb.SolverConfig(tolerance=1e-5), "homogenized", spec["levels"], 0.4)
+        # SIMP iteration 1 untimed: builds the hierarchy and captures the PCG
+        # iteration graph (one-time setup of a run of hundreds of iterations)
+        R.solve(problem.model)
+        R.design_step(problem.model)
         times, its = [], []
         for it in range(a.simp_iters):
             model = problem.model
@@ -259,11 +263,14 @@ def run_ours(a):
             R.design_step(model)
         solve = {"s_per_simp_iter": sum(times) / len(times), "simp_iters": a.simp_iters, "cg_iters": its,
                  "ms_per_cg_iter": 1e3 * sum(times) / max(1, sum(its)), "levels": R.hier.n_levels,
-                 "note": "first SIMP iterations of the cfg design loop (refresh + homogenized MGPCG, "
-                         "V(1,1), tol 1e-5, warm start)"}
+                 "note": "SIMP iterations 2..%d of the cfg design loop (each: refresh + homogenized MGPCG, "
+                         "V(1,1), tol 1e-5, warm start; iteration 1 untimed: hierarchy build + graph "
+                         "capture)" % (a.simp_iters + 1)}
         # the reference's default coarse scheme (stored Galerkin element matrices)
         del R
         R = DeviceRun(problem, opt, vb.SolverConfig(tolerance=1e-5), "galerkin", spec["levels"], 0.4)
+        R.solve(problem.model)
+        R.design_step(problem.model)
         times, its = [], []
         for it in range(a.simp_iters):
             barrier()
@@ -275,8 +282,8 @@ def run_ours(a):
             R.design_step(problem.model)
         solve_galerkin = {"s_per_simp_iter": sum(times) / len(times), "simp_iters": a.simp_iters,
                           "cg_iters": its, "ms_per_cg_iter": 1e3 * sum(times) / max(1, sum(its)),
-                          "note": "same iterations with scheme='galerkin' (the reference default): refresh "
-                                  "builds the coarse element matrices"}
+                          "note": "same iterations with scheme='galerkin' (the reference default; refresh "
+                                  "builds the coarse element matrices, level 1 matrix-free)"}
         del R
     elif a.simp_iters > 0:
         # the same design iterations on the slabs (SlabRun: refresh + slab MGPCG, then the
@@ -285,6 +292,8 @@ def run_ours(a):
 
         opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
         R = SlabRun.from_process_group(problem, opt, vb.SolverConfig(tolerance=1e-5), spec["levels"], 0.4)
+        R.solve(problem.model)  # iteration 1 untimed (graph capture, communicator warm-up)
+        R.design_step(problem.model)
         times, its = [], []
         for it in range(a.simp_iters):
             barrier()
@@ -297,8 +306,8 @@ def run_ours(a):
         solve = {"s_per_simp_iter": sum(times) / len(times), "simp_iters": a.simp_iters, "cg_iters": its,
                  "ms_per_cg_iter": 1e3 * sum(times) / max(1, sum(its)), "levels": R.S.levels,
                  "dist_level": R.S.plan.dist_level,
-                 "note": "first SIMP iterations on z-slabs (refresh + slab MGPCG, V(1,1), tol 1e-5, warm "
-                         "start; design step distributed too), max over ranks"}
+                 "note": "SIMP iterations 2..%d on z-slabs (refresh + slab MGPCG, V(1,1), tol 1e-5, warm "
+                         "start; design step distributed too), max over ranks" % (a.simp_iters + 1)}
         R.S.close()
 
     res = {
