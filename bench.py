@@ -47,6 +47,7 @@ def _args():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--simp-iters", type=int, default=4, help="SIMP iterations timed for the solve figure")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 single-GPU section")
     ap.add_argument("--slabs", action="store_true",
                     help="use the z-slab/NCCL path even at N=1 (under torchrun; smoke test of the transport)")
     return ap.parse_args()
@@ -342,6 +343,9 @@ def run_ours(a):
     }
     if solve_galerkin is not None:
         res["solve_galerkin"] = solve_galerkin
+    if not slabs and not a.no_cfg5 and a.config == "cfg2":
+        del state, u, v
+        res["cfg5_single_gpu"] = cfg5_section(vb, DeviceRun, lib, ptr, stream_ptr)
     if rank == 0 and world == 1 and not a.no_cpu:
         res["cpu_baseline"] = cpu_baseline(a.config, reps=2)
     if slabs:
@@ -349,6 +353,55 @@ def run_ours(a):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(res))
+
+
+def cfg5_section(vb, DeviceRun, lib, ptr, stream_ptr):
+    """BASELINE cfg5 (768x384x384: 113M elements, 342M dofs) on ONE B200: K(rho)u
+    (CUDA events, device-resident) and SIMP iterations 2-3 end to end."""
+    import numpy as np
+    import torch
+
+    from paper_2201_12931_b200 import cases
+
+    prob = cases.cantilever(768, 384, 384)
+    g = prob.grid
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * g.h, ch_tol=1e-12)
+    R = DeviceRun(prob, opt, vb.SolverConfig(tolerance=1e-5), "homogenized", None, 0.4)
+    R._set_scale(prob.model)
+    d = R.d
+    rng = np.random.default_rng(0)
+    u = d.upload(rng.standard_normal(g.n_dofs) * (~R.fixed_mask))
+    v = d.zeros()
+    sp = stream_ptr()
+    for _ in range(3):
+        lib.vt_apply_projected(d.handle, ptr(R.scale), ptr(u), ptr(v), sp)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(10):
+        lib.vt_apply_projected(d.handle, ptr(R.scale), ptr(u), ptr(v), sp)
+    e1.record(s)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) * 1e-4
+    del u, v
+    alg = 16.0 * g.n_dofs + 8.0 * g.n_elements
+    hbm, _ = _peaks()
+    R.solve(prob.model)  # iteration 1: hierarchy + graph capture (untimed)
+    R.design_step(prob.model)
+    its, secs = [], []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        ts = time.perf_counter()
+        rep = R.solve(prob.model)
+        R.design_step(prob.model)
+        torch.cuda.synchronize()
+        secs.append(time.perf_counter() - ts)
+        its.append(rep.iterations)
+    return {"workload": "cfg5 cantilever 768x384x384, 113246208 elements, 341955075 dofs, 1 GPU",
+            "apply_ms": t * 1e3, "apply_gdofs": g.n_dofs / t / 1e9, "roofline_frac": alg / t / 1e9 / hbm,
+            "simp_iter_s": sum(secs) / len(secs), "cg_iters": its,
+            "ms_per_cg_iter": 1e3 * sum(secs) / max(1, sum(its)),
+            "note": "SIMP iterations 2-3 (refresh + homogenized MGPCG + design step, device resident)"}
 
 
 # ---------------------------------------------------------------------- CPU baseline
