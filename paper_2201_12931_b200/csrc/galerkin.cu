@@ -521,7 +521,7 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
     VT_TRY(launch_hex8(F, H8_APPLY, false, H->scale[0], H->gfa, nullptr, nullptr, H->gfb, 0.0,
                        nullptr, stop, s));
     VT_TRY(launch_restrict(F, G, H->gfb, H->gc1, stop, -1, -1, s));
-    const int grid_n = G->nsm * 4;
+    const int grid_n = fit_grid((long long)(G->g.pB - G->g.pA) * (G->g.ny + 1) * (G->g.nx + 1), GL_THREADS, G->nsm * 4);
     if (mode == 0)
       launch_pdl(gal_vec_epilogue_kernel<0>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gc1, u, f, H->gdiag[l], H->omega, out, stop);
     else if (mode == 1)
@@ -535,7 +535,7 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
   const long long nel = (long long)G->g.nx * G->g.ny * G->g.nz;
   const int grid_e = (int)std::min<long long>((nel * 32 + GL_THREADS - 1) / GL_THREADS, (long long)G->nsm * 16);
   launch_pdl(gal_elem_kernel, grid_e, GL_THREADS, 0, s, G->g, G->mask, H->mats[l], u, H->gve, stop);
-  const int grid_n = G->nsm * 4;
+  const int grid_n = fit_grid((long long)(G->g.pB - G->g.pA) * (G->g.ny + 1) * (G->g.nx + 1), GL_THREADS, G->nsm * 4);
   if (mode == 0)
     launch_pdl(gal_node_kernel<0>, grid_n, GL_THREADS, 0, s, G->g, G->mask, H->gve, u, f, H->gdiag[l], H->omega, out, stop);
   else if (mode == 1)
@@ -549,7 +549,7 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
 
 vt_status gal_jacobi0(vt_hier* H, int l, const double* f, double* u, const int* stop, cudaStream_t s) {
   vt_grid* G = H->lv[l];
-  launch_pdl(gal_jacobi0_kernel, G->nsm * 4, GL_THREADS, 0, s, G->g, G->mask, f, H->gdiag[l], H->omega, u, stop);
+  launch_pdl(gal_jacobi0_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * (G->g.ny + 1) * (G->g.nx + 1), GL_THREADS, G->nsm * 4), GL_THREADS, 0, s, G->g, G->mask, f, H->gdiag[l], H->omega, u, stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;

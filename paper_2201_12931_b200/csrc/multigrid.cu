@@ -220,7 +220,7 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
     ke = C->g.k1 + C->g.last;
   }
   if (ke <= kb) return VT_OK;
-  launch_pdl(restrict_kernel, C->nsm * 4, MG_THREADS, 0, s, F->g, C->g, C->mask, rf, fc, stop, kb, ke);
+  launch_pdl(restrict_kernel, fit_grid((long long)(ke - kb) * (C->g.ny + 1) * (C->g.nx + 1), MG_THREADS, C->nsm * 4), MG_THREADS, 0, s, F->g, C->g, C->mask, rf, fc, stop, kb, ke);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -315,10 +315,16 @@ __global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double
 }
 
 static size_t prolong_smem(const Geom& gc) { return (size_t)4 * (gc.nx + 1) * 3 * sizeof(double); }
+// one CTA per coarse (row, plane) unit covering the fine slab's owned planes
+static int prolong_grid(const Geom& gc, const Geom& gf, int cap) {
+  const int fk0 = gf.k0 + gf.pA - 1, fk1 = gf.k0 + gf.pB - 1;
+  const int K0 = fk0 >> 1, K1 = ((fk1 - 1) >> 1) + 1;
+  return fit_grid((long long)(K1 - K0) * (gc.ny + 1), 1, cap);
+}
 
 vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
                              const int* stop, cudaStream_t s) {
-  launch_pdl(prolong_kernel<true>, F->nsm * 8, MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
+  launch_pdl(prolong_kernel<true>, prolong_grid(C->g, F->g, F->nsm * 8), MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -326,7 +332,7 @@ vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* u
 
 vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
                              cudaStream_t s) {
-  launch_pdl(prolong_kernel<false>, F->nsm * 8, MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
+  launch_pdl(prolong_kernel<false>, prolong_grid(C->g, F->g, F->nsm * 8), MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -589,7 +595,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
   }
   for (int l = L - 2; l >= top; --l) {
     vt_grid* G = H->lv[l];
-    launch_pdl(prolong_kernel<true>, G->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, G->g, G->mask,
+    launch_pdl(prolong_kernel<true>, prolong_grid(H->lv[l + 1]->g, G->g, G->nsm * 8), MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, G->g, G->mask,
                                                            ucur[l + 1], ucur[l], stop);
     count_launch();
     VT_CUDA(cudaGetLastError());
@@ -806,7 +812,7 @@ vt_status vt_hier_prolong(vt_hier* H, int l, const double* coarse, double* fine,
   cudaStream_t s = (cudaStream_t)stream;
   if (l < 0 || l + 1 >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
   vt_grid* F = H->lv[l];
-  launch_pdl(prolong_kernel<false>, F->nsm * 8, MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, F->g, F->mask, coarse,
+  launch_pdl(prolong_kernel<false>, prolong_grid(H->lv[l + 1]->g, F->g, F->nsm * 8), MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, F->g, F->mask, coarse,
                                                           fine, nullptr);
   count_launch();
   VT_CUDA(cudaGetLastError());

@@ -36,7 +36,7 @@ __global__ void project_kernel(Geom g, const uint8_t* mask, const double* src, d
 }
 
 vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_t s) {
-  launch_pdl(project_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, G->mask, src, dst);
+  launch_pdl(project_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * G->g.nplane / 3, VT_THREADS, G->nsm * 8), VT_THREADS, 0, s, G->g, G->mask, src, dst);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -106,7 +106,7 @@ __global__ void zero_owned_kernel(Geom g, double* v) {
     v[i] = 0.0;
 }
 vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s) {
-  launch_pdl(zero_owned_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, v);
+  launch_pdl(zero_owned_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * G->g.nplane, VT_THREADS, G->nsm * 8), VT_THREADS, 0, s, G->g, v);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -244,7 +244,7 @@ __global__ void jacobi0_kernel(Geom g, const uint8_t* __restrict__ mask,
 
 vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const double* f,
                          double* u, const int* stop, cudaStream_t s) {
-  launch_pdl(jacobi0_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, G->mask, scale, G->coef.kd, omega, f, u,
+  launch_pdl(jacobi0_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * (G->g.ny + 1) * ((G->g.nx + 2) / 2), VT_THREADS, G->nsm * 8), VT_THREADS, 0, s, G->g, G->mask, scale, G->coef.kd, omega, f, u,
                                                    stop);
   count_launch();
   VT_CUDA(cudaGetLastError());
@@ -439,7 +439,7 @@ vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, c
 }
 vt_status launch_copy(vt_grid* G, const int* skip, const double* src, double* dst,
                       cudaStream_t s) {
-  launch_pdl(copy_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, skip, src, dst);
+  launch_pdl(copy_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * G->g.nplane, VT_THREADS, G->nsm * 8), VT_THREADS, 0, s, G->g, skip, src, dst);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;

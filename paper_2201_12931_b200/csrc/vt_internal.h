@@ -31,6 +31,14 @@ vt_status cuda_fail(cudaError_t e, const char* what);
 extern unsigned long long g_launches;  // kernels launched by this library
 extern bool g_pdl;                     // launch with programmatic stream serialization (VT_PDL=0 off)
 
+// grid for `work` independent items of `per_cta` each, capped (small coarse
+// levels would otherwise launch a full-GPU grid of mostly idle CTAs)
+inline int fit_grid(long long work, long long per_cta, int cap) {
+  long long g = (work + per_cta - 1) / per_cta;
+  if (g < 1) g = 1;
+  return (int)(g < cap ? g : cap);
+}
+
 template <typename... ExpTypes, typename... ActTypes>
 inline cudaError_t launch_pdl(void (*kernel)(ExpTypes...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t s, ActTypes&&... args) {
