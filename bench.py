@@ -440,6 +440,9 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from paper_2201_12931_b200.cases import CONFIGS
+
+    nx, ny, nz = CONFIGS[a.config]["dims"]
     fn, n = _oracle_apply_setup(a.config)
     for _ in range(a.warmup):
         fn()
@@ -454,7 +457,10 @@ def run_reference(a):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (rho ~ U(0,1), u ~ N(0,1), seed 0)",
-        "config": {"workload": f"{a.config} cantilever, reference CPU K(rho)u (numpy oracle port)"},
+        "config": {"workload": f"{a.config} cantilever {nx}x{ny}x{nz} hex8 matrix-free K(rho)u, {n} dofs, "
+                               f"{nx * ny * nz} elements", "dofs": n, "elements": nx * ny * nz,
+                   "parallelism": f"{cores} host cores (numpy/OpenBLAS)",
+                   "implementation": "reference algorithm, CPU (oracle/cpu_path.py port of operator.py:58-81)"},
         "cpu_baseline": {"value": v, "unit": "GDOF/s", "cores": cores, "kind": "port",
                          "sample": f"{a.steps} timed applications on the full {a.config} grid"},
         "e2e": {"value": v, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
