@@ -223,7 +223,7 @@ static vt_status dist_vcycle(vt_dist* D, const std::vector<const double*>& f0, c
     std::vector<double*> uu(NL), rr(NL);
     for (int i = 0; i < NL; ++i) {
       DSlab& S = D->sl[i];
-      VT_TRY(launch_jacobi0(S.lv[l], S.scale[l], D->omega, fl(i, l), S.u[l], stop, s));
+      VT_TRY(launch_jacobi0w(S.lv[l], S.wd[l], fl(i, l), S.u[l], stop, s));
       ucur[l][i] = S.u[l];
       uu[i] = S.u[l];
       rr[i] = S.r[l];
@@ -447,10 +447,12 @@ vt_status vt_dist_create(vt_dist** out, int nx, int ny, int nz, double h, double
     const int NLv = dist_level + 1;
     S.u.assign(NLv, nullptr); S.u2.assign(NLv, nullptr); S.r.assign(NLv, nullptr);
     S.f.assign(NLv, nullptr); S.scale.assign(NLv, nullptr); S.rho.assign(NLv, nullptr);
+    S.wd.assign(NLv, nullptr);
     for (int l = 0; l < NLv; ++l) {
       vt_grid* G = S.lv[l];
       const size_t vl = G->vec_len(), el = G->elem_len();
       if ((st = alloc_zero(&S.u[l], vl)) || (st = alloc_zero(&S.u2[l], vl)) ||
+          (st = alloc_zero(&S.wd[l], vl)) ||
           (st = alloc_zero(&S.r[l], vl)) || (st = alloc_zero(&S.f[l], vl)) ||
           (st = alloc_zero(&S.scale[l], el)) || (st = alloc_zero(&S.rho[l], G->nel_local())))
         return bail(st);
@@ -505,7 +507,7 @@ vt_status vt_dist_destroy(vt_dist* D) {
     for (size_t l = 0; l < S.lv.size(); ++l) {
       if (l < S.u.size()) {
         cudaFree(S.u[l]); cudaFree(S.u2[l]); cudaFree(S.r[l]); cudaFree(S.f[l]);
-        cudaFree(S.scale[l]); cudaFree(S.rho[l]);
+        cudaFree(S.scale[l]); cudaFree(S.rho[l]); cudaFree(S.wd[l]);
       }
       vt_grid_destroy(S.lv[l]);
     }
@@ -574,6 +576,8 @@ vt_status vt_dist_refresh(vt_dist* D, const double* const* rho, const double* co
     }
     VT_TRY(halo_elems(D, l, e, s));
   }
+  for (int l = 0; l <= D->D; ++l)
+    for (DSlab& S : D->sl) VT_TRY(launch_wdiag(S.lv[l], S.scale[l], D->omega, S.wd[l], s));
   // gather level-D densities into the replicated full grid (slab = contiguous range)
   const long long per_layer = (long long)(D->nx >> D->D) * (D->ny >> D->D);
   if (!D->remote()) {

@@ -34,6 +34,7 @@ struct DSlab {
   int rank = 0;
   std::vector<vt_grid*> lv;                       // levels 0..D (slab geometry)
   std::vector<double*> u, u2, r, f, scale, rho;   // per level; f[0] unused
+  std::vector<double*> wd;                        // omega / diag per dof (refresh)
   double *x = nullptr, *fv = nullptr, *rr = nullptr, *p = nullptr, *q = nullptr, *t = nullptr;
   const double* z = nullptr;                      // V-cycle output buffer (level 0)
   int tkb = 0, tke = 0;                           // tail-level coarse planes restricted here

@@ -18,6 +18,14 @@
 namespace vt {
 
 constexpr int MG_THREADS = 256;
+#ifndef VT_MG_R
+#define VT_MG_R 6
+#endif
+constexpr int MG_R = VT_MG_R;  // rows in flight per thread in the transfer kernels
+#ifndef VT_MG_CPS
+#define VT_MG_CPS 4
+#endif
+constexpr int MG_CPS = VT_MG_CPS;  // transfer-kernel CTAs per SM (grid cap)
 
 __device__ __forceinline__ bool node_coords(const Geom& g, long long t, int& p, int& j, int& i) {
   i = (int)(t % (g.nx + 1));
@@ -126,88 +134,117 @@ __global__ void count_fixed_kernel(Geom g, const uint8_t* m, unsigned long long*
 //   dst[i] = (src[2i] + 0.5 src[2i+1]) + 0.5 src[2i-1]   (missing terms skipped)
 // Coarse node planes [kb, ke) (global); a z-slab of the fine level restricts
 // into the planes whose centre fine plane 2K it owns (its ghost planes hold
-// the neighbours' residual planes 2K0-1 and 2K1-1+1).  One thread per coarse
-// node reads each of its 9 fine rows as two 16-byte-aligned node pairs
-// (2I-2, 2I-1) and (2I, 2I+1) -- 6 vector loads instead of 27 scalar ones --
-// and combines them in the reference's pass order (bit-identical).
-__global__ void restrict_kernel(Geom gf, Geom gc, const uint8_t* mc, const double* __restrict__ rf,
-                                double* __restrict__ fc, const int* stop, int kb, int ke) {
+// the neighbours' residual planes 2K0-1 and 2K1-1+1).
+//
+// A CTA takes a block of RJ coarse rows x RI coarse nodes of one coarse plane
+// K.  Phase 1 streams the (2 RJ + 1) fine rows x (2 RI + 1) fine nodes of the
+// three fine planes 2K, 2K+1, 2K-1 with coalesced row loads and keeps their
+// z-pass combination in shared memory; phase 2 computes each coarse dof from
+// 9 staged values (y pass, then x pass).  Every fine value is read from L2
+// ~1.6 times (the plane 2K+1 is shared with K+1) instead of through 16-byte
+// gathers at a 48-byte stride (3 L1 wavefronts per useful sector).  Same pass
+// order and rounding as the reference: bit-identical.
+constexpr int RJ = 8, RI_MAX = 42;  // 3 (2 RI + 1) <= 256 staged dofs per row: one per thread
+
+struct RestrictBlk {
+  int nJb, nIb, RI;  // blocks per plane in y / x, coarse nodes per x block
+};
+static RestrictBlk restrict_blocks(const Geom& gc) {
+  RestrictBlk b;
+  b.nJb = (gc.ny + 1 + RJ - 1) / RJ;
+  b.nIb = (gc.nx + 1 + RI_MAX - 1) / RI_MAX;
+  b.RI = (gc.nx + 1 + b.nIb - 1) / b.nIb;
+  return b;
+}
+static size_t restrict_smem(const RestrictBlk& b) { return (size_t)(2 * RJ + 1) * (2 * b.RI + 1) * 3 * sizeof(double); }
+
+// Threads own row positions (a fine dof column of the staged block, then a
+// coarse dof column) and walk the rows, so the index arithmetic is per column
+// and every row step is one coalesced load per plane.
+__global__ void __launch_bounds__(MG_THREADS)
+    restrict_kernel(Geom gf, Geom gc, const uint8_t* __restrict__ mc, const double* __restrict__ rf,
+                    double* __restrict__ fc, const int* stop, int kb, int ke, RestrictBlk blk) {
   griddep_wait();
   if (stop && *(volatile const int*)stop) return;
-  const long long nn = (long long)(ke - kb) * (gc.ny + 1) * (gc.nx + 1);
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int I = (int)(t % (gc.nx + 1));
-    const long long rr = t / (gc.nx + 1);
-    const int J = (int)(rr % (gc.ny + 1));
-    const int K = (int)(rr / (gc.ny + 1)) + kb;
+  extern __shared__ double tzs[];  // [2 RJ + 1][3 (2 RI + 1)]
+  const int W = 3 * (2 * blk.RI + 1);
+  const long long units = (long long)(ke - kb) * blk.nJb * blk.nIb;
+  const long long rowpitch = (long long)gf.rp * 3;
+  for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const int ib = (int)(unit % blk.nIb);
+    const long long r0 = unit / blk.nIb;
+    const int jb = (int)(r0 % blk.nJb);
+    const int K = (int)(r0 / blk.nJb) + kb;
+    const int J0 = jb * RJ, I0 = ib * blk.RI;
+    const int nJ = min(RJ, gc.ny + 1 - J0), nI = min(blk.RI, gc.nx + 1 - I0);
+    // staged fine rows y0 .. y0 + nrow - 1, clipped to [0, ny]
+    const int y0 = 2 * J0 - 1;
+    const int ya = max(y0, 0), yb = min(y0 + 2 * nJ + 1, gf.ny + 1);
+    const bool ok1 = 2 * K + 1 <= gf.nz, ok2 = K >= 1;
+    const double* pl0 = rf + node_off(gf, 2 * K - gf.k0 + 1, 0, 0) * 3;
+    const double* pl1 = ok1 ? pl0 + gf.nplane : pl0;
+    const double* pl2 = ok2 ? pl0 - gf.nplane : pl0;
+    __syncthreads();
+    // phase 1: z pass of the staged fine rows
+    const int wn = 3 * (2 * nI + 1);
+    for (int e = threadIdx.x; e < wn; e += blockDim.x) {
+      const int xd = 3 * (2 * I0 - 1) + e;  // fine dof index within the row
+      if (xd < 0 || xd >= 3 * (gf.nx + 1)) continue;
+      for (int y = ya; y < yb; y += MG_R) {
+        double a0[MG_R], a1[MG_R], a2[MG_R];
+#pragma unroll
+        for (int k = 0; k < MG_R; ++k) {
+          if (y + k >= yb) break;
+          const long long o = (y + k) * rowpitch + xd;
+          a0[k] = pl0[o];
+          a1[k] = pl1[o];
+          a2[k] = pl2[o];
+        }
+#pragma unroll
+        for (int k = 0; k < MG_R; ++k) {
+          if (y + k >= yb) break;
+          double v = a0[k];
+          if (ok1) v = __dadd_rn(v, 0.5 * a1[k]);
+          if (ok2) v = __dadd_rn(v, 0.5 * a2[k]);
+          tzs[(y + k - y0) * W + e] = v;
+        }
+      }
+    }
+    __syncthreads();
+    // phase 2: y pass then x pass per coarse dof
     const int p = K - gc.k0 + 1;
-    const long long cnode = node_off(gc, p, J, I);
-    const unsigned m = mc[mask_off(gc, p, J, I)];
-    const int fj[3] = {2 * J, 2 * J + 1, 2 * J - 1};
-    const int fk[3] = {2 * K, 2 * K + 1, 2 * K - 1};
-    bool okj[3], oki[3], okk[3];
+    const int cw = 3 * nI;
+    for (int e = threadIdx.x; e < cw; e += blockDim.x) {
+      const int ii = e / 3, c = e - 3 * ii;
+      const int I = I0 + ii;
+      const bool oki1 = 2 * I + 1 <= gf.nx, oki2 = I >= 1;
+      double* out = fc + node_off(gc, p, J0, I) * 3 + c;
+      const uint8_t* mrow = mc + mask_off(gc, p, J0, I);
+#pragma unroll 2
+      for (int jj = 0; jj < nJ; ++jj) {
+        const int J = J0 + jj;
+        const bool okj1 = 2 * J + 1 <= gf.ny, okj2 = J >= 1;
+        // staged row of fine y = 2J + d is 2 jj + 1 + d; node x = 2I + d is 2 ii + 1 + d
+        const double* rw = tzs + (2 * jj + 1) * W + 3 * (2 * ii + 1) + c;
+        double ty[3];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      okj[q] = fj[q] >= 0 && fj[q] <= gf.ny;
-      okk[q] = fk[q] >= 0 && fk[q] <= gf.nz;
-    }
-    oki[0] = true;
-    oki[1] = 2 * I + 1 <= gf.nx;
-    oki[2] = I >= 1;
-    // tz[a][b][c]: after the z pass, fine row a (y), fine column b (x), component c
-    double tz[3][3][3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) tz[a][b][c] = 0.0;
-      if (!okj[a]) continue;
-      double row[3][12];  // per z row: nodes 2I-2, 2I-1, 2I, 2I+1 (x 3 comps)
-#pragma unroll
-      for (int z = 0; z < 3; ++z) {
-        if (!okk[z]) continue;
-        const double2* q = reinterpret_cast<const double2*>(
-            rf + node_off(gf, fk[z] - gf.k0 + 1, fj[a], 2 * I) * 3);
-        double2 v0 = q[0], v1 = q[1], v2 = q[2];
-        row[z][6] = v0.x; row[z][7] = v0.y; row[z][8] = v1.x;
-        row[z][9] = v1.y; row[z][10] = v2.x; row[z][11] = v2.y;
-        if (I >= 1) {
-          v0 = q[-3]; v1 = q[-2]; v2 = q[-1];
-          row[z][0] = v0.x; row[z][1] = v0.y; row[z][2] = v1.x;
-          row[z][3] = v1.y; row[z][4] = v2.x; row[z][5] = v2.y;
+        for (int b = 0; b < 3; ++b) {
+          const int dx = b == 0 ? 0 : (b == 1 ? 3 : -3);
+          if ((b == 1 && !oki1) || (b == 2 && !oki2)) {
+            ty[b] = 0.0;
+            continue;
+          }
+          double v = rw[dx];
+          if (okj1) v = __dadd_rn(v, 0.5 * rw[W + dx]);
+          if (okj2) v = __dadd_rn(v, 0.5 * rw[-W + dx]);
+          ty[b] = v;
         }
+        double v = ty[0];
+        if (oki1) v = __dadd_rn(v, 0.5 * ty[1]);
+        if (oki2) v = __dadd_rn(v, 0.5 * ty[2]);
+        const unsigned m = mrow[(long long)jj * gc.mp];
+        out[(long long)jj * gc.rp * 3] = ((m >> c) & 1u) ? 0.0 : v;
       }
-      // x column b -> node slot in row[][]: centre 2I = 2, +1 = 3, -1 = 1
-      const int slot[3] = {2, 3, 1};
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        if (!oki[b]) continue;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int o = slot[b] * 3 + c;
-          double v = row[0][o];
-          if (okk[1]) v = __dadd_rn(v, 0.5 * row[1][o]);
-          if (okk[2]) v = __dadd_rn(v, 0.5 * row[2][o]);
-          tz[a][b][c] = v;
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double ty[3];
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        double v = tz[0][b][c];
-        if (okj[1]) v = __dadd_rn(v, 0.5 * tz[1][b][c]);
-        if (okj[2]) v = __dadd_rn(v, 0.5 * tz[2][b][c]);
-        ty[b] = v;
-      }
-      double v = ty[0];
-      if (oki[1]) v = __dadd_rn(v, 0.5 * ty[1]);
-      if (oki[2]) v = __dadd_rn(v, 0.5 * ty[2]);
-      fc[cnode * 3 + c] = ((m >> c) & 1u) ? 0.0 : v;
     }
   }
 }
@@ -220,7 +257,17 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
     ke = C->g.k1 + C->g.last;
   }
   if (ke <= kb) return VT_OK;
-  launch_pdl(restrict_kernel, fit_grid((long long)(ke - kb) * (C->g.ny + 1) * (C->g.nx + 1), MG_THREADS, C->nsm * 4), MG_THREADS, 0, s, F->g, C->g, C->mask, rf, fc, stop, kb, ke);
+  const RestrictBlk blk = restrict_blocks(C->g);
+  const size_t sm = restrict_smem(blk);
+  static bool attr = false;
+  if (!attr) {
+    VT_CUDA(cudaFuncSetAttribute(restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)((2 * RJ + 1) * (2 * RI_MAX + 1) * 3 * sizeof(double))));
+    attr = true;
+  }
+  const long long units = (long long)(ke - kb) * blk.nJb * blk.nIb;
+  launch_pdl(restrict_kernel, fit_grid(units, 1, C->nsm * MG_CPS), MG_THREADS, sm, s, F->g, C->g,
+             (const uint8_t*)C->mask, rf, fc, stop, kb, ke, blk);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -228,103 +275,123 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
 
 // u_f (+)= P u_c with fine fixed dofs zeroed in P u_c.  Per axis (z, y, x):
 //   even: dst = src[i/2];  odd: dst = 0.5 * (src[(i-1)/2] + src[(i+1)/2])
-// A CTA takes one coarse row pair unit (J, K): it stages the coarse rows
-// (J..J+1) x (K..K+1) in shared memory with coalesced loads and writes the
-// fine rows (2J..2J+1) x (2K..2K+1) with one thread per fine dof, so every
-// global access is contiguous (the node-per-thread gather was load-issue and
-// sector bound at 3 doubles per node).  Same z -> y -> x pass order and
-// rounding as the reference: bit-identical.  A slab produces exactly the fine
-// planes it owns (coarse plane K covers fine planes 2K, 2K+1).
+// A CTA takes a block of PJ coarse rows x PI coarse nodes of one coarse plane
+// K: it stages the coarse values of planes K, K+1, rows J0..J0+PJ, nodes
+// I0..I0+PI in shared memory, then updates the fine dofs of planes 2K, 2K+1,
+// rows 2J0.., nodes 2I0.. with one thread per fine dof along each row (every
+// global access contiguous; the read-modify-writes unrolled for memory-level
+// parallelism).  Same z -> y -> x pass order and rounding as the reference:
+// bit-identical.  A slab produces exactly the fine planes it owns.
+constexpr int PJ = 8, PI_MAX = 42;  // 6 PI <= 256 fine dofs per row: one per thread
+
+struct ProlongBlk {
+  int K0, K1;        // coarse planes covering the fine slab's owned planes
+  int nJb, nIb, PI;  // blocks per plane in y / x, coarse nodes per x block
+};
+static ProlongBlk prolong_blocks(const Geom& gc, const Geom& gf) {
+  ProlongBlk b;
+  const int fk0 = gf.k0 + gf.pA - 1, fk1 = gf.k0 + gf.pB - 1;
+  b.K0 = fk0 >> 1;
+  b.K1 = ((fk1 - 1) >> 1) + 1;
+  b.nJb = (gc.ny + 1 + PJ - 1) / PJ;
+  b.nIb = (gc.nx + 1 + PI_MAX - 1) / PI_MAX;
+  b.PI = (gc.nx + 1 + b.nIb - 1) / b.nIb;
+  return b;
+}
+static size_t prolong_smem(const ProlongBlk& b) { return (size_t)2 * (PJ + 1) * (b.PI + 1) * 3 * sizeof(double); }
+
 template <bool ADD>
-__global__ void prolong_kernel(Geom gc, Geom gf, const uint8_t* mf, const double* __restrict__ uc,
-                               double* __restrict__ uf, const int* stop) {
+__global__ void __launch_bounds__(MG_THREADS)
+    prolong_kernel(Geom gc, Geom gf, const uint8_t* __restrict__ mf, const double* __restrict__ uc,
+                   double* __restrict__ uf, const int* stop, ProlongBlk blk) {
   griddep_wait();
   if (stop && *(volatile const int*)stop) return;
-  extern __shared__ double sc[];                        // [kz][jy][cw]
-  const int fk0 = gf.k0 + gf.pA - 1;                    // first owned fine plane
-  const int fk1 = gf.k0 + gf.pB - 1;                    // one past the last
-  const int K0 = fk0 >> 1, K1 = ((fk1 - 1) >> 1) + 1;   // coarse planes covering them
-  const int cy = gc.ny + 1;
-  const int cw = (gc.nx + 1) * 3, fw = (gf.nx + 1) * 3;
-  const int units = (K1 - K0) * cy;
-  for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
-    const int K = K0 + unit / cy, J = unit % cy;
-    const int J1 = J + 1 <= gc.ny ? J + 1 : J, Kp = K + 1 <= gc.nz ? K + 1 : K;
+  extern __shared__ double sc[];  // [kz 2][PJ + 1][3 (PI + 1)]
+  const int fk0 = gf.k0 + gf.pA - 1, fk1 = gf.k0 + gf.pB - 1;
+  const int SW = 3 * (blk.PI + 1), SP = (PJ + 1) * SW;
+  const long long units = (long long)(blk.K1 - blk.K0) * blk.nJb * blk.nIb;
+  const long long rowpitch = (long long)gf.rp * 3;
+  for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const int ib = (int)(unit % blk.nIb);
+    const long long r0 = unit / blk.nIb;
+    const int jb = (int)(r0 % blk.nJb);
+    const int K = (int)(r0 / blk.nJb) + blk.K0;
+    const int J0 = jb * PJ, I0 = ib * blk.PI;
+    const int nJ = min(PJ, gc.ny + 1 - J0), nI = min(blk.PI, gc.nx + 1 - I0);
+    // staged coarse rows J0..J0+nJ, nodes I0..I0+nI (clipped to the grid)
+    const int sJ = min(nJ + 1, gc.ny + 1 - J0), sw = 3 * min(nI + 1, gc.nx + 1 - I0);
+    const int Kp = K + 1 <= gc.nz ? K + 1 : K;
     __syncthreads();
-    for (int t = threadIdx.x; t < 4 * cw; t += blockDim.x) {
-      const int q = t / cw, e = t - q * cw;
-      const int kk = (q >> 1) ? Kp : K, jj = (q & 1) ? J1 : J;
-      sc[t] = uc[node_off(gc, kk - gc.k0 + 1, jj, 0) * 3 + e];
+    for (int t = threadIdx.x; t < 2 * sJ * sw; t += blockDim.x) {
+      const int r = t / sw, e = t - r * sw;
+      const int kz = r / sJ, jj = r - kz * sJ;
+      sc[kz * SP + jj * SW + e] = uc[node_off(gc, (kz ? Kp : K) - gc.k0 + 1, J0 + jj, I0) * 3 + e];
     }
     __syncthreads();
-    // the 4 fine rows (2J+b2, 2K+c) of this unit; every dof of a row is
-    // handled together with the same dof of the other rows, so each thread
-    // has 4 independent read-modify-writes in flight
-    double* rowp[4];
-    const uint8_t* mrow[4];
-    bool ok[4];
+    // fine planes 2K + cz (owned), rows 2 J0 + ry (<= ny), dofs 3 (2 I0) + e
+    const int fy0 = 2 * J0, fx0 = 2 * I0;
+    const int nfy = min(2 * nJ, gf.ny + 1 - fy0), nfx = min(2 * nI, gf.nx + 1 - fx0);
+    const int czb = (2 * K >= fk0) ? 0 : 1;
+    const int cze = (2 * K + 1 < fk1 && 2 * K + 1 <= gf.nz) ? 2 : 1;
+    for (int e = threadIdx.x; e < 3 * nfx; e += blockDim.x) {
+      const int ix = e / 3, comp = e - 3 * ix;
+      const int ixx = ix >> 1, ox = ix & 1;
+      for (int cz = czb; cz < cze; ++cz) {
+        const int pf = 2 * K + cz - gf.k0 + 1;
+        double* urow = uf + node_off(gf, pf, fy0, fx0) * 3 + e;
+        const uint8_t* mrow = mf + mask_off(gf, pf, fy0, fx0 + ix);
+        const double* s0 = sc + 3 * ixx + comp + (cz ? SP : 0);
+        for (int ry0 = 0; ry0 < nfy; ry0 += MG_R) {
+          double old[MG_R];
+          unsigned mk[MG_R];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = q >> 1, b2 = q & 1;
-      const int fk = 2 * K + c, fj = 2 * J + b2;
-      ok[q] = fk >= fk0 && fk < fk1 && fj <= gf.ny;
-      const int pf = fk - gf.k0 + 1;
-      rowp[q] = ok[q] ? uf + node_off(gf, pf, fj, 0) * 3 : uf;
-      mrow[q] = ok[q] ? mf + mask_off(gf, pf, fj, 0) : mf;
-    }
-    for (int d = threadIdx.x; d < fw; d += blockDim.x) {
-      const int i = d / 3, comp = d - 3 * i;
-      const int I = i >> 1;
-      double old[4];
-      unsigned mk[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        old[q] = (ADD && ok[q]) ? rowp[q][d] : 0.0;
-        mk[q] = ok[q] ? mrow[q][i] : 0u;
-      }
-      // coarse corner values at x = I (and I+1): zc[kz][jy][ix]
-      double zc[2][2][2];
-#pragma unroll
-      for (int kz = 0; kz < 2; ++kz)
-#pragma unroll
-        for (int jy = 0; jy < 2; ++jy) {
-          zc[kz][jy][0] = sc[(kz * 2 + jy) * cw + I * 3 + comp];
-          zc[kz][jy][1] = (i & 1) ? sc[(kz * 2 + jy) * cw + (I + 1) * 3 + comp] : 0.0;
-        }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (!ok[q]) continue;
-        const int c = q >> 1, b2 = q & 1;
-        double y[2];
-#pragma unroll
-        for (int ix = 0; ix < 2; ++ix) {
-          double z0 = zc[0][0][ix], z1 = zc[0][1][ix];
-          if (c) {  // z pass
-            z0 = 0.5 * __dadd_rn(z0, zc[1][0][ix]);
-            z1 = 0.5 * __dadd_rn(z1, zc[1][1][ix]);
+          for (int k = 0; k < MG_R; ++k) {
+            if (ry0 + k >= nfy) break;
+            old[k] = ADD ? urow[(ry0 + k) * rowpitch] : 0.0;
+            mk[k] = mrow[(long long)(ry0 + k) * gf.mp];
           }
-          y[ix] = b2 ? 0.5 * __dadd_rn(z0, z1) : z0;  // y pass
+#pragma unroll
+          for (int k = 0; k < MG_R; ++k) {
+            const int ry = ry0 + k;
+            if (ry >= nfy) break;
+            const int jy = ry >> 1, oy = ry & 1;
+            const double* q = s0 + jy * SW;
+            double y[2];
+#pragma unroll
+            for (int xx = 0; xx < 2; ++xx) {
+              if (xx && !ox) {
+                y[1] = 0.0;
+                continue;
+              }
+              // z pass (staged plane K+1 minus plane K is SP; z-odd rows average them)
+              double z0 = q[3 * xx], z1 = oy ? q[SW + 3 * xx] : 0.0;
+              if (cz) {
+                z0 = 0.5 * __dadd_rn(q[3 * xx - SP], z0);
+                if (oy) z1 = 0.5 * __dadd_rn(q[SW + 3 * xx - SP], z1);
+              }
+              y[xx] = oy ? 0.5 * __dadd_rn(z0, z1) : z0;  // y pass
+            }
+            double v = y[0];
+            if (ox) v = 0.5 * __dadd_rn(v, y[1]);  // x pass
+            if ((mk[k] >> comp) & 1u) v = 0.0;
+            urow[ry * rowpitch] = ADD ? __dadd_rn(old[k], v) : v;
+          }
         }
-        double v = y[0];
-        if (i & 1) v = 0.5 * __dadd_rn(v, y[1]);  // x pass
-        if ((mk[q] >> comp) & 1u) v = 0.0;
-        rowp[q][d] = ADD ? __dadd_rn(old[q], v) : v;
       }
     }
   }
 }
 
-static size_t prolong_smem(const Geom& gc) { return (size_t)4 * (gc.nx + 1) * 3 * sizeof(double); }
-// one CTA per coarse (row, plane) unit covering the fine slab's owned planes
-static int prolong_grid(const Geom& gc, const Geom& gf, int cap) {
-  const int fk0 = gf.k0 + gf.pA - 1, fk1 = gf.k0 + gf.pB - 1;
-  const int K0 = fk0 >> 1, K1 = ((fk1 - 1) >> 1) + 1;
-  return fit_grid((long long)(K1 - K0) * (gc.ny + 1), 1, cap);
+// one CTA per coarse (plane, row block, node block) unit covering the fine slab's owned planes
+static int prolong_grid(const ProlongBlk& b, int cap) {
+  return fit_grid((long long)(b.K1 - b.K0) * b.nJb * b.nIb, 1, cap);
 }
 
 vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
                              const int* stop, cudaStream_t s) {
-  launch_pdl(prolong_kernel<true>, prolong_grid(C->g, F->g, F->nsm * 8), MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
+  const ProlongBlk b = prolong_blocks(C->g, F->g);
+  launch_pdl(prolong_kernel<true>, prolong_grid(b, F->nsm * MG_CPS), MG_THREADS, prolong_smem(b), s, C->g,
+             F->g, (const uint8_t*)F->mask, uc, uf, stop, b);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -332,7 +399,9 @@ vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* u
 
 vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
                              cudaStream_t s) {
-  launch_pdl(prolong_kernel<false>, prolong_grid(C->g, F->g, F->nsm * 8), MG_THREADS, prolong_smem(C->g), s, C->g, F->g, F->mask, uc, uf, stop);
+  const ProlongBlk b = prolong_blocks(C->g, F->g);
+  launch_pdl(prolong_kernel<false>, prolong_grid(b, F->nsm * MG_CPS), MG_THREADS, prolong_smem(b), s, C->g,
+             F->g, (const uint8_t*)F->mask, uc, uf, stop, b);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -574,7 +643,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
       if (gal(l))
         VT_TRY(gal_jacobi0(H, l, fl[l], H->u[l], stop, s));
       else
-        VT_TRY(launch_jacobi0(G, H->scale[l], H->omega, fl[l], H->u[l], stop, s));
+        VT_TRY(launch_jacobi0w(G, H->wd[l], fl[l], H->u[l], stop, s));
       for (int k = 1; k < H->sweeps; ++k) VT_TRY(smooth(l, false));
       if (gal(l))
         VT_TRY(gal_level_op(H, l, 1, ucur[l], fl[l], H->r[l], stop, s));
@@ -595,10 +664,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
   }
   for (int l = L - 2; l >= top; --l) {
     vt_grid* G = H->lv[l];
-    launch_pdl(prolong_kernel<true>, prolong_grid(H->lv[l + 1]->g, G->g, G->nsm * 8), MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, G->g, G->mask,
-                                                           ucur[l + 1], ucur[l], stop);
-    count_launch();
-    VT_CUDA(cudaGetLastError());
+    VT_TRY(launch_prolong_add(H->lv[l + 1], G, ucur[l + 1], ucur[l], stop, s));
     for (int k = 0; k < H->sweeps; ++k) VT_TRY(smooth(l, want_rz && l == 0 && k == H->sweeps - 1));
   }
   *z_out = ucur[top];
@@ -671,6 +737,10 @@ vt_status vt_hier_create_ex(vt_hier** out, vt_grid* fine, int n_levels, double o
     VT_CUDA(cudaMemset(H->scale[l], 0, G->elem_len() * sizeof(double)));
     VT_CUDA(cudaMalloc(&H->rho[l], (size_t)G->nel_local() * sizeof(double)));
   }
+  // damped inverse diagonals of the smoothed homogenized-operator levels
+  H->wd.assign(L, nullptr);
+  for (int l = 0; l + 1 < L; ++l)
+    if (l == 0 || H->scheme == 0) VT_TRY(hier_alloc_vec(H->lv[l], &H->wd[l]));
   vt_grid* C = H->lv.back();
   H->nL = (int)(3LL * (C->g.nx + 1) * (C->g.ny + 1) * (C->g.nz + 1));
   H->scheme = scheme;
@@ -689,6 +759,7 @@ vt_status vt_hier_destroy(vt_hier* H) {
     cudaFree(H->u[l]); cudaFree(H->u2[l]); cudaFree(H->r[l]);
     if (l > 0) cudaFree(H->f[l]);
     cudaFree(H->scale[l]); cudaFree(H->rho[l]);
+    if (l < H->wd.size()) cudaFree(H->wd[l]);
     if (l > 0) vt_grid_destroy(H->lv[l]);
   }
   gal_free(H);
@@ -736,6 +807,8 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
       VT_TRY(launch_scale(c, H->rho[l], p, kmin, E, H->scale[l], bad, s));
     }
   }
+  for (int l = 0; l < L; ++l)
+    if (H->wd[l]) VT_TRY(launch_wdiag(H->lv[l], H->scale[l], H->omega, H->wd[l], s));
   // coarsest direct factor
   vt_grid* C = H->lv.back();
   const int n = H->nL;
@@ -812,11 +885,7 @@ vt_status vt_hier_prolong(vt_hier* H, int l, const double* coarse, double* fine,
   cudaStream_t s = (cudaStream_t)stream;
   if (l < 0 || l + 1 >= (int)H->lv.size()) return fail(VT_EINVAL, "level out of range");
   vt_grid* F = H->lv[l];
-  launch_pdl(prolong_kernel<false>, prolong_grid(H->lv[l + 1]->g, F->g, F->nsm * 8), MG_THREADS, prolong_smem(H->lv[l + 1]->g), s, H->lv[l + 1]->g, F->g, F->mask, coarse,
-                                                          fine, nullptr);
-  count_launch();
-  VT_CUDA(cudaGetLastError());
-  return VT_OK;
+  return launch_prolong_set(H->lv[l + 1], F, coarse, fine, nullptr, s);
 }
 
 vt_status vt_hier_jacobi(vt_hier* H, int l, const double* u, const double* f, int sweeps,

@@ -9,6 +9,7 @@
 namespace vt {
 
 constexpr int VT_THREADS = 256;
+constexpr int EW_B = 4;  // elements in flight per thread in the streaming kernels
 
 int dot_grid(vt_grid* G) { return G->nsm * 4; }
 
@@ -251,6 +252,79 @@ vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const do
   return VT_OK;
 }
 
+// Damped inverse diagonal per dof, w = omega / d (0 on fixed dofs and row
+// pads), computed once per refresh so the first Jacobi sweep of every V-cycle
+// is a pure stream u = w f (diag assembly in the reference corner order,
+// operator.py:116-124; one rounding of omega/d shared with the smoother
+// epilogue, see hex8_apply.cu).
+__global__ void wdiag_kernel(Geom g, const uint8_t* __restrict__ mask,
+                             const double* __restrict__ scale, double kd, double omega,
+                             double* __restrict__ w) {
+  griddep_wait();
+  const long long nn = (long long)(g.pB - g.pA) * (g.ny + 1) * (g.nx + 1);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (g.nx + 1));
+    const long long r = t / (g.nx + 1);
+    const int j = (int)(r % (g.ny + 1));
+    const int p = (int)(r / (g.ny + 1)) + g.pA;
+    const long long node = node_off(g, p, j, i);
+    const double wv = __ddiv_rn(omega, node_diag(g, scale, p, j, i, kd));
+    const unsigned m = mask[mask_off(g, p, j, i)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[node * 3 + c] = ((m >> c) & 1u) ? 0.0 : wv;
+  }
+}
+
+vt_status launch_wdiag(vt_grid* G, const double* scale, double omega, double* w, cudaStream_t s) {
+  VT_CUDA(cudaMemsetAsync(w, 0, G->vec_len() * sizeof(double), s));
+  launch_pdl(wdiag_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, (const uint8_t*)G->mask, scale,
+             G->coef.kd, omega, w);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// u = w f over the owned node planes (first damped Jacobi sweep from zero,
+// multigrid.py:387-393); 16-byte accesses, fully coalesced.
+__global__ void jacobi0w_kernel(long long n2, const double2* __restrict__ w,
+                                const double2* __restrict__ f, double2* __restrict__ u,
+                                const int* stop) {
+  griddep_wait();
+  if (stop && *(volatile const int*)stop) return;
+  const long long st = (long long)gridDim.x * blockDim.x;
+  for (long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; t0 < n2; t0 += EW_B * st) {
+    double2 a[EW_B], b[EW_B];
+#pragma unroll
+    for (int k = 0; k < EW_B; ++k) {
+      const long long t = t0 + k * st;
+      if (t < n2) {
+        a[k] = w[t];
+        b[k] = f[t];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < EW_B; ++k) {
+      const long long t = t0 + k * st;
+      if (t < n2)
+        u[t] = make_double2(a[k].x == 0.0 ? 0.0 : __dmul_rn(a[k].x, b[k].x),
+                            a[k].y == 0.0 ? 0.0 : __dmul_rn(a[k].y, b[k].y));
+    }
+  }
+}
+
+vt_status launch_jacobi0w(vt_grid* G, const double* w, const double* f, double* u, const int* stop,
+                          cudaStream_t s) {
+  const long long a = (long long)G->g.pA * G->g.nplane, b = (long long)G->g.pB * G->g.nplane;
+  const long long n2 = (b - a) / 2;  // nplane is even (rp even)
+  launch_pdl(jacobi0w_kernel, fit_grid(n2, VT_THREADS * EW_B, G->nsm * 8), VT_THREADS, 0, s, n2,
+             reinterpret_cast<const double2*>(w + a), reinterpret_cast<const double2*>(f + a),
+             reinterpret_cast<double2*>(u + a), stop);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 // ---------------------------------------------------------------- PCG passes
 // x += alpha p ; r -= alpha q ; partial ||r||^2   [ref: solver.py:131-136]
 // (16-byte vector accesses: owned ranges start and end on even indices)
@@ -273,21 +347,37 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
   const double2* q2 = reinterpret_cast<const double2*>(q + b);
   const long long n2 = (e - b) / 2;
   double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double2 pv = p2[i];
-    double2 xv = x2[i];
-    xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
-    xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
-    x2[i] = xv;
-    if (with_r) {
-      const double2 qv = q2[i];
-      double2 rv = r2[i];
-      rv.x = __dsub_rn(rv.x, __dmul_rn(alpha, qv.x));
-      rv.y = __dsub_rn(rv.y, __dmul_rn(alpha, qv.y));
-      r2[i] = rv;
-      acc = fma(rv.x, rv.x, acc);
-      acc = fma(rv.y, rv.y, acc);
+  // EW_B independent elements per thread in flight (same per-thread element
+  // order as a plain grid-stride loop, so the partial sums are unchanged)
+  const long long st = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n2; i0 += EW_B * st) {
+    double2 pv[EW_B], xv[EW_B], qv[EW_B], rv[EW_B];
+#pragma unroll
+    for (int k = 0; k < EW_B; ++k) {
+      const long long i = i0 + k * st;
+      if (i < n2) {
+        pv[k] = p2[i];
+        xv[k] = x2[i];
+        if (with_r) {
+          qv[k] = q2[i];
+          rv[k] = r2[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < EW_B; ++k) {
+      const long long i = i0 + k * st;
+      if (i >= n2) break;
+      xv[k].x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
+      xv[k].y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
+      x2[i] = xv[k];
+      if (with_r) {
+        rv[k].x = __dsub_rn(rv[k].x, __dmul_rn(alpha, qv[k].x));
+        rv[k].y = __dsub_rn(rv[k].y, __dmul_rn(alpha, qv[k].y));
+        r2[i] = rv[k];
+        acc = fma(rv[k].x, rv[k].x, acc);
+        acc = fma(rv[k].y, rv[k].y, acc);
+      }
     }
   }
   if (with_r) {
@@ -307,13 +397,25 @@ __global__ void pcg_xpby_kernel(Geom g, const PcgCtl* ctl, const double* __restr
   const double2* z2 = reinterpret_cast<const double2*>(z + b);
   double2* p2 = reinterpret_cast<double2*>(p + b);
   const long long n2 = (e - b) / 2;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double2 zv = z2[i];
-    double2 pv = p2[i];
-    pv.x = __dadd_rn(zv.x, __dmul_rn(beta, pv.x));
-    pv.y = __dadd_rn(zv.y, __dmul_rn(beta, pv.y));
-    p2[i] = pv;
+  const long long st = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n2; i0 += EW_B * st) {
+    double2 zv[EW_B], pv[EW_B];
+#pragma unroll
+    for (int k = 0; k < EW_B; ++k) {
+      const long long i = i0 + k * st;
+      if (i < n2) {
+        zv[k] = z2[i];
+        pv[k] = p2[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < EW_B; ++k) {
+      const long long i = i0 + k * st;
+      if (i >= n2) break;
+      pv[k].x = __dadd_rn(zv[k].x, __dmul_rn(beta, pv[k].x));
+      pv[k].y = __dadd_rn(zv[k].y, __dmul_rn(beta, pv[k].y));
+      p2[i] = pv[k];
+    }
   }
 }
 

@@ -130,6 +130,7 @@ struct vt_hier {
   double *A = nullptr, *W = nullptr, *Kinv = nullptr, *k0l = nullptr;
   double* A0 = nullptr;             // assembled coarsest matrix (refinement residual)
   double* cvec = nullptr;           // 3 dense coarsest vectors: fc, x0, r
+  std::vector<double*> wd;          // omega / diag per dof (0 on fixed), smoothed levels
   int* status = nullptr;
   bool factored = false;
   const double* last_z = nullptr;  // buffer that holds the V-cycle output

@@ -37,5 +37,8 @@ vt_status launch_pcg_s3(PcgCtl* c, const double* partial, int n, cudaStream_t s)
 vt_status launch_pcg_s4(PcgCtl* c, const double* partial, int n, int counts, cudaStream_t s);
 vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const double* f,
                          double* u, const int* stop, cudaStream_t s);
+vt_status launch_wdiag(vt_grid* G, const double* scale, double omega, double* w, cudaStream_t s);
+vt_status launch_jacobi0w(vt_grid* G, const double* w, const double* f, double* u, const int* stop,
+                          cudaStream_t s);
 
 }  // namespace vt

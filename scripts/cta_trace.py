@@ -23,10 +23,12 @@ v = d.zeros()
 lib.vt_debug_trace(d.handle, 1, None, 0)
 for _ in range(5):
     lib.vt_apply_projected(d.handle, ptr(st.scale_dev), ptr(u), ptr(v), stream_ptr())
-ncta = 148
-buf = np.zeros(4 * ncta, dtype=np.uint64)
-lib.vt_debug_trace(d.handle, 1, buf.ctypes.data_as(C.c_void_p), ncta)
+buf = np.zeros(4 * 4096, dtype=np.uint64)
+lib.vt_debug_trace(d.handle, 1, buf.ctypes.data_as(C.c_void_p), 4096)
 rec = buf.reshape(-1, 4).astype(np.int64)
+rec = rec[rec[:, 0] > 0]
+ncta = rec.shape[0]
+print("grid", ncta, "SMs used", len(np.unique(rec[:, 2])))
 t0 = rec[:, 0].min()
 start, end = (rec[:, 0] - t0) / 1e3, (rec[:, 1] - t0) / 1e3
 dur = end - start

@@ -89,6 +89,25 @@ def _hier(g, tag):
     return st, vb.build_hierarchy(grid, st, int(g[f"{tag}_levels"]), scheme="homogenized")
 
 
+@pytest.mark.parametrize("dims", [(264, 36, 12), (128, 16, 8), (4, 4, 4)])
+def test_transfers_bit_identical_across_blocks(dims):
+    """Restriction / prolongation stay bit-identical to the axis passes when the
+    coarse level spans several (row block, node block) units of the staged
+    kernels (multigrid.py:341-371)."""
+    nx, ny, nz = dims
+    rng = np.random.default_rng(7)
+    fm = face_fixed_mask(nx, ny, nz)
+    grid = vb.build_grid(nx, ny, nz, 1.0)
+    st = vb.OperatorState(grid, rng.uniform(0.1, 1.0, grid.n_elements), vb.MaterialModel(), fm)
+    H = vb.build_hierarchy(grid, st, 3, scheme="homogenized")
+    OH = O.hier_build((nz, ny, nx), 1.0, fm, H.n_levels)
+    for l in range(H.n_levels - 1):
+        rf = rng.standard_normal(H.levels[l].n_dofs)
+        assert np.array_equal(H.restrict(l, rf), O.restrict(OH, l, rf)), l
+        ec = rng.standard_normal(H.levels[l + 1].n_dofs)
+        assert np.array_equal(H.prolongate(l, ec), O.prolong(OH, l, ec)), l
+
+
 @pytest.mark.parametrize("tag", ["t", "v", "w"])
 def test_multigrid_matches_reference(tag):
     g = golden("multigrid.npz")
