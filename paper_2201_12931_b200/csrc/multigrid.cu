@@ -616,8 +616,11 @@ vt_status launch_coarse_solve(vt_hier* H, const double* f, double* u, const int*
 // level `top` with right-hand side f0 (top > 0: the replicated coarse tail of a
 // z-slab hierarchy, whose level-`top` residual the slabs restricted into
 // H->f[top]; see dist.cu).
+// fused_j0: the PCG control block when pcg_update already wrote the level-0
+// first Jacobi sweep into H->u[0] (see pcg_update_kernel)
 vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, double* rz_partial,
-                             bool want_rz, cudaStream_t s, const double** z_out, int top) {
+                             bool want_rz, cudaStream_t s, const double** z_out, int top,
+                             const PcgCtl* fused_j0) {
   const int L = (int)H->lv.size();
   std::vector<const double*> fl(L);
   std::vector<double*> ucur(L);
@@ -643,7 +646,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
       if (gal(l))
         VT_TRY(gal_jacobi0(H, l, fl[l], H->u[l], stop, s));
       else
-        VT_TRY(launch_jacobi0w(G, H->wd[l], fl[l], H->u[l], stop, s));
+        VT_TRY(launch_jacobi0w(G, H->wd[l], fl[l], H->u[l], stop, s, l == 0 ? fused_j0 : nullptr));
       for (int k = 1; k < H->sweeps; ++k) VT_TRY(smooth(l, false));
       if (gal(l))
         VT_TRY(gal_level_op(H, l, 1, ucur[l], fl[l], H->r[l], stop, s));

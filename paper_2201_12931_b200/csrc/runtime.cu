@@ -441,7 +441,12 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
                           &ctl->stop, s)) != VT_OK) break;
     if ((st = launch_pcg_s1(ctl, P0, h8g, s)) != VT_OK) break;
     // x += alpha p ; r -= alpha q | r = f - K x       [ref: solver.py:131-136]
-    if ((st = launch_pcg_update(G, ctl, G->w_x, G->w_p, G->w_r, G->w_q, P1, 1, s)) != VT_OK) break;
+    // (MG preconditioner: the same pass writes the V-cycle's first Jacobi sweep)
+    static const bool fuse_env = !getenv("VT_FUSE_J0") || atoi(getenv("VT_FUSE_J0")) != 0;
+    const bool fuse_j0 = fuse_env && precond == 2 && H->lv.size() >= 2 && H->sweeps >= 1 && H->wd[0];
+    if ((st = launch_pcg_update(G, ctl, G->w_x, G->w_p, G->w_r, G->w_q, P1, 1, s,
+                                fuse_j0 ? H->wd[0] : nullptr, fuse_j0 ? H->u[0] : nullptr)) != VT_OK)
+      break;
     if ((st = launch_pcg_update(G, ctl, G->w_x, G->w_p, G->w_r, G->w_q, P1, 0, s)) != VT_OK) break;
     if ((st = launch_hex8(G, H8_RESID, true, scale, G->w_x, G->w_x, G->w_f, G->w_r, 0.0, P1,
                           &ctl->skip_true50, s)) != VT_OK) break;
@@ -455,7 +460,9 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
     const double* z = G->w_z;
     int nrz = dg;
     if (precond == 2) {
-      if ((st = hier_vcycle_launch(H, G->w_r, &ctl->stop, P3, true, s, &z)) != VT_OK) break;
+      if ((st = hier_vcycle_launch(H, G->w_r, &ctl->stop, P3, true, s, &z, 0,
+                                   fuse_j0 ? ctl : nullptr)) != VT_OK)
+        break;
       nrz = hier_rz_parts(H);
       if (nrz == 0) {
         if ((st = launch_dot(G, G->w_r, z, P3, &nrz, s, &ctl->stop)) != VT_OK) break;

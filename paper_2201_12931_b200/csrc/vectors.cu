@@ -289,9 +289,12 @@ vt_status launch_wdiag(vt_grid* G, const double* scale, double omega, double* w,
 // multigrid.py:387-393); 16-byte accesses, fully coalesced.
 __global__ void jacobi0w_kernel(long long n2, const double2* __restrict__ w,
                                 const double2* __restrict__ f, double2* __restrict__ u,
-                                const int* stop) {
+                                const int* stop, const PcgCtl* fused) {
   griddep_wait();
   if (stop && *(volatile const int*)stop) return;
+  // already produced by this iteration's pcg_update, unless r was replaced
+  // by a true residual (skip_rec: periodic one; !skip_swap: candidate copy)
+  if (fused && !fused->skip_rec && fused->skip_swap) return;
   const long long st = (long long)gridDim.x * blockDim.x;
   for (long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; t0 < n2; t0 += EW_B * st) {
     double2 a[EW_B], b[EW_B];
@@ -314,12 +317,12 @@ __global__ void jacobi0w_kernel(long long n2, const double2* __restrict__ w,
 }
 
 vt_status launch_jacobi0w(vt_grid* G, const double* w, const double* f, double* u, const int* stop,
-                          cudaStream_t s) {
+                          cudaStream_t s, const PcgCtl* fused) {
   const long long a = (long long)G->g.pA * G->g.nplane, b = (long long)G->g.pB * G->g.nplane;
   const long long n2 = (b - a) / 2;  // nplane is even (rp even)
   launch_pdl(jacobi0w_kernel, fit_grid(n2, VT_THREADS * EW_B, G->nsm * 8), VT_THREADS, 0, s, n2,
              reinterpret_cast<const double2*>(w + a), reinterpret_cast<const double2*>(f + a),
-             reinterpret_cast<double2*>(u + a), stop);
+             reinterpret_cast<double2*>(u + a), stop, fused);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -328,9 +331,14 @@ vt_status launch_jacobi0w(vt_grid* G, const double* w, const double* f, double* 
 // ---------------------------------------------------------------- PCG passes
 // x += alpha p ; r -= alpha q ; partial ||r||^2   [ref: solver.py:131-136]
 // (16-byte vector accesses: owned ranges start and end on even indices)
+// With w != nullptr (MG-preconditioned solves) the same pass also writes the
+// V-cycle's first damped Jacobi sweep u0 = w r of the updated residual
+// (multigrid.py:387-393), which the V-cycle then skips unless r was replaced
+// by a true residual this iteration (jacobi0w_kernel's ctl test).
 __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict__ x,
                                   const double* __restrict__ p, double* __restrict__ r,
-                                  const double* __restrict__ q, double* partial, int with_r) {
+                                  const double* __restrict__ q, double* partial, int with_r,
+                                  const double* __restrict__ w, double* __restrict__ u0) {
   griddep_wait();
   __shared__ double red[VT_THREADS / 32];
   // The host enqueues iteration k+1 before it sees that iteration k stopped, so
@@ -345,13 +353,16 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
   const double2* p2 = reinterpret_cast<const double2*>(p + b);
   double2* r2 = reinterpret_cast<double2*>(r + b);
   const double2* q2 = reinterpret_cast<const double2*>(q + b);
+  const double2* w2 = reinterpret_cast<const double2*>(w + b);
+  double2* u2 = reinterpret_cast<double2*>(u0 + b);
+  const bool fuse = with_r && w != nullptr;
   const long long n2 = (e - b) / 2;
   double acc = 0.0;
   // EW_B independent elements per thread in flight (same per-thread element
   // order as a plain grid-stride loop, so the partial sums are unchanged)
   const long long st = (long long)gridDim.x * blockDim.x;
   for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n2; i0 += EW_B * st) {
-    double2 pv[EW_B], xv[EW_B], qv[EW_B], rv[EW_B];
+    double2 pv[EW_B], xv[EW_B], qv[EW_B], rv[EW_B], wv[EW_B];
 #pragma unroll
     for (int k = 0; k < EW_B; ++k) {
       const long long i = i0 + k * st;
@@ -362,6 +373,7 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
           qv[k] = q2[i];
           rv[k] = r2[i];
         }
+        if (fuse) wv[k] = w2[i];
       }
     }
 #pragma unroll
@@ -377,6 +389,9 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
         r2[i] = rv[k];
         acc = fma(rv[k].x, rv[k].x, acc);
         acc = fma(rv[k].y, rv[k].y, acc);
+        if (fuse)
+          u2[i] = make_double2(wv[k].x == 0.0 ? 0.0 : __dmul_rn(wv[k].x, rv[k].x),
+                               wv[k].y == 0.0 ? 0.0 : __dmul_rn(wv[k].y, rv[k].y));
       }
     }
   }
@@ -527,8 +542,10 @@ __global__ void pcg_s4_kernel(PcgCtl* c, const double* partial, int n, int count
 }
 
 vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p, double* r,
-                            const double* q, double* partial, int with_r, cudaStream_t s) {
-  launch_pdl(pcg_update_kernel, dot_grid(G), VT_THREADS, 0, s, G->g, ctl, x, p, r, q, partial, with_r);
+                            const double* q, double* partial, int with_r, cudaStream_t s,
+                            const double* w, double* u0) {
+  launch_pdl(pcg_update_kernel, dot_grid(G), VT_THREADS, 0, s, G->g, ctl, x, p, r, q, partial, with_r,
+             w, u0);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;

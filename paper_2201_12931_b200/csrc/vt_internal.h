@@ -169,8 +169,10 @@ vt_status launch_diag(vt_grid* G, const double* scale, double* d, cudaStream_t s
 vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s);
 int dot_grid(vt_grid* G);
 // (multigrid.cu)
+struct PcgCtl;
 vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, double* rz_partial,
-                             bool want_rz, cudaStream_t s, const double** z_out, int top = 0);
+                             bool want_rz, cudaStream_t s, const double** z_out, int top = 0,
+                             const PcgCtl* fused_j0 = nullptr);
 int hier_rz_parts(vt_hier* H);
 vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
                              const int* stop, cudaStream_t s);

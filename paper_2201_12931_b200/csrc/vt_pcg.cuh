@@ -24,7 +24,8 @@ struct PcgCtl {
 };
 
 vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p, double* r,
-                            const double* q, double* partial, int with_r, cudaStream_t s);
+                            const double* q, double* partial, int with_r, cudaStream_t s,
+                            const double* w = nullptr, double* u0 = nullptr);
 vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s);
 vt_status launch_copy(vt_grid* G, const int* skip, const double* src, double* dst,
                       cudaStream_t s);
@@ -39,6 +40,6 @@ vt_status launch_jacobi0(vt_grid* G, const double* scale, double omega, const do
                          double* u, const int* stop, cudaStream_t s);
 vt_status launch_wdiag(vt_grid* G, const double* scale, double omega, double* w, cudaStream_t s);
 vt_status launch_jacobi0w(vt_grid* G, const double* w, const double* f, double* u, const int* stop,
-                          cudaStream_t s);
+                          cudaStream_t s, const PcgCtl* fused = nullptr);
 
 }  // namespace vt
