@@ -144,19 +144,27 @@ __global__ void count_fixed_kernel(Geom g, const uint8_t* m, unsigned long long*
 // ~1.6 times (the plane 2K+1 is shared with K+1) instead of through 16-byte
 // gathers at a 48-byte stride (3 L1 wavefronts per useful sector).  Same pass
 // order and rounding as the reference: bit-identical.
-constexpr int RJ = 8, RI_MAX = 42;  // 3 (2 RI + 1) <= 256 staged dofs per row: one per thread
+constexpr int RJ_MAX = 8, RI_MAX = 42;  // 3 (2 RI + 1) <= 256 staged dofs per row: one per thread
 
 struct RestrictBlk {
-  int nJb, nIb, RI;  // blocks per plane in y / x, coarse nodes per x block
+  int nJb, nIb, RI, RJ;  // blocks per plane in y / x, coarse nodes per x block, rows per block
 };
-static RestrictBlk restrict_blocks(const Geom& gc) {
+// row blocks as tall as possible while the launch still has ~4 units per SM
+// (small coarse levels would otherwise walk rows serially in a few CTAs)
+static int transfer_rows(int planes, int rows, int nIb, int nsm) {
+  int r = RJ_MAX;
+  while (r > 1 && (long long)planes * ((rows + r - 1) / r) * nIb < 4LL * nsm) r /= 2;
+  return r;
+}
+static RestrictBlk restrict_blocks(const Geom& gc, int kb, int ke, int nsm) {
   RestrictBlk b;
-  b.nJb = (gc.ny + 1 + RJ - 1) / RJ;
   b.nIb = (gc.nx + 1 + RI_MAX - 1) / RI_MAX;
   b.RI = (gc.nx + 1 + b.nIb - 1) / b.nIb;
+  b.RJ = transfer_rows(ke - kb, gc.ny + 1, b.nIb, nsm);
+  b.nJb = (gc.ny + 1 + b.RJ - 1) / b.RJ;
   return b;
 }
-static size_t restrict_smem(const RestrictBlk& b) { return (size_t)(2 * RJ + 1) * (2 * b.RI + 1) * 3 * sizeof(double); }
+static size_t restrict_smem(const RestrictBlk& b) { return (size_t)(2 * b.RJ + 1) * (2 * b.RI + 1) * 3 * sizeof(double); }
 
 // Threads own row positions (a fine dof column of the staged block, then a
 // coarse dof column) and walk the rows, so the index arithmetic is per column
@@ -175,8 +183,8 @@ __global__ void __launch_bounds__(MG_THREADS)
     const long long r0 = unit / blk.nIb;
     const int jb = (int)(r0 % blk.nJb);
     const int K = (int)(r0 / blk.nJb) + kb;
-    const int J0 = jb * RJ, I0 = ib * blk.RI;
-    const int nJ = min(RJ, gc.ny + 1 - J0), nI = min(blk.RI, gc.nx + 1 - I0);
+    const int J0 = jb * blk.RJ, I0 = ib * blk.RI;
+    const int nJ = min(blk.RJ, gc.ny + 1 - J0), nI = min(blk.RI, gc.nx + 1 - I0);
     // staged fine rows y0 .. y0 + nrow - 1, clipped to [0, ny]
     const int y0 = 2 * J0 - 1;
     const int ya = max(y0, 0), yb = min(y0 + 2 * nJ + 1, gf.ny + 1);
@@ -257,12 +265,12 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
     ke = C->g.k1 + C->g.last;
   }
   if (ke <= kb) return VT_OK;
-  const RestrictBlk blk = restrict_blocks(C->g);
+  const RestrictBlk blk = restrict_blocks(C->g, kb, ke, C->nsm);
   const size_t sm = restrict_smem(blk);
   static bool attr = false;
   if (!attr) {
     VT_CUDA(cudaFuncSetAttribute(restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)((2 * RJ + 1) * (2 * RI_MAX + 1) * 3 * sizeof(double))));
+                                 (int)((2 * RJ_MAX + 1) * (2 * RI_MAX + 1) * 3 * sizeof(double))));
     attr = true;
   }
   const long long units = (long long)(ke - kb) * blk.nJb * blk.nIb;
@@ -278,27 +286,31 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
 // A CTA takes a block of PJ coarse rows x PI coarse nodes of one coarse plane
 // K: it stages the coarse values of planes K, K+1, rows J0..J0+PJ, nodes
 // I0..I0+PI in shared memory, then updates the fine dofs of planes 2K, 2K+1,
-// rows 2J0.., nodes 2I0.. with one thread per fine dof along each row (every
-// global access contiguous; the read-modify-writes unrolled for memory-level
-// parallelism).  Same z -> y -> x pass order and rounding as the reference:
-// bit-identical.  A slab produces exactly the fine planes it owns.
-constexpr int PJ = 8, PI_MAX = 42;  // 6 PI <= 256 fine dofs per row: one per thread
+// rows 2J0.., nodes 2I0..  A thread owns one fine dof column and walks the
+// coarse rows: the z pass of coarse row jy+1 is formed once and serves fine
+// rows 2jy (even) and 2jy+1 (odd, with row jy's carried value); every global
+// access is contiguous along the row, read-modify-writes batched.  Same
+// z -> y -> x pass order and rounding as the reference: bit-identical.  A
+// slab produces exactly the fine planes it owns.
+constexpr int PJ_MAX = 8, PI_MAX = 42;  // 6 PI <= 256 fine dofs per row: one per thread
+constexpr int PR_B = 3;                  // coarse rows (6 fine rows) per batch of read-modify-writes
 
 struct ProlongBlk {
-  int K0, K1;        // coarse planes covering the fine slab's owned planes
-  int nJb, nIb, PI;  // blocks per plane in y / x, coarse nodes per x block
+  int K0, K1;            // coarse planes covering the fine slab's owned planes
+  int nJb, nIb, PI, PJ;  // blocks per plane in y / x, coarse nodes per x block, rows per block
 };
-static ProlongBlk prolong_blocks(const Geom& gc, const Geom& gf) {
+static ProlongBlk prolong_blocks(const Geom& gc, const Geom& gf, int nsm) {
   ProlongBlk b;
   const int fk0 = gf.k0 + gf.pA - 1, fk1 = gf.k0 + gf.pB - 1;
   b.K0 = fk0 >> 1;
   b.K1 = ((fk1 - 1) >> 1) + 1;
-  b.nJb = (gc.ny + 1 + PJ - 1) / PJ;
   b.nIb = (gc.nx + 1 + PI_MAX - 1) / PI_MAX;
   b.PI = (gc.nx + 1 + b.nIb - 1) / b.nIb;
+  b.PJ = transfer_rows(b.K1 - b.K0, gc.ny + 1, b.nIb, nsm);
+  b.nJb = (gc.ny + 1 + b.PJ - 1) / b.PJ;
   return b;
 }
-static size_t prolong_smem(const ProlongBlk& b) { return (size_t)2 * (PJ + 1) * (b.PI + 1) * 3 * sizeof(double); }
+static size_t prolong_smem(const ProlongBlk& b) { return (size_t)2 * (b.PJ + 1) * (b.PI + 1) * 3 * sizeof(double); }
 
 template <bool ADD>
 __global__ void __launch_bounds__(MG_THREADS)
@@ -308,7 +320,7 @@ __global__ void __launch_bounds__(MG_THREADS)
   if (stop && *(volatile const int*)stop) return;
   extern __shared__ double sc[];  // [kz 2][PJ + 1][3 (PI + 1)]
   const int fk0 = gf.k0 + gf.pA - 1, fk1 = gf.k0 + gf.pB - 1;
-  const int SW = 3 * (blk.PI + 1), SP = (PJ + 1) * SW;
+  const int SW = 3 * (blk.PI + 1), SP = (blk.PJ + 1) * SW;
   const long long units = (long long)(blk.K1 - blk.K0) * blk.nJb * blk.nIb;
   const long long rowpitch = (long long)gf.rp * 3;
   for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
@@ -316,8 +328,8 @@ __global__ void __launch_bounds__(MG_THREADS)
     const long long r0 = unit / blk.nIb;
     const int jb = (int)(r0 % blk.nJb);
     const int K = (int)(r0 / blk.nJb) + blk.K0;
-    const int J0 = jb * PJ, I0 = ib * blk.PI;
-    const int nJ = min(PJ, gc.ny + 1 - J0), nI = min(blk.PI, gc.nx + 1 - I0);
+    const int J0 = jb * blk.PJ, I0 = ib * blk.PI;
+    const int nJ = min(blk.PJ, gc.ny + 1 - J0), nI = min(blk.PI, gc.nx + 1 - I0);
     // staged coarse rows J0..J0+nJ, nodes I0..I0+nI (clipped to the grid)
     const int sJ = min(nJ + 1, gc.ny + 1 - J0), sw = 3 * min(nI + 1, gc.nx + 1 - I0);
     const int Kp = K + 1 <= gc.nz ? K + 1 : K;
@@ -335,46 +347,48 @@ __global__ void __launch_bounds__(MG_THREADS)
     const int cze = (2 * K + 1 < fk1 && 2 * K + 1 <= gf.nz) ? 2 : 1;
     for (int e = threadIdx.x; e < 3 * nfx; e += blockDim.x) {
       const int ix = e / 3, comp = e - 3 * ix;
-      const int ixx = ix >> 1, ox = ix & 1;
+      const bool ox = ix & 1;
+      const double* col = sc + 3 * (ix >> 1) + comp;
       for (int cz = czb; cz < cze; ++cz) {
         const int pf = 2 * K + cz - gf.k0 + 1;
         double* urow = uf + node_off(gf, pf, fy0, fx0) * 3 + e;
         const uint8_t* mrow = mf + mask_off(gf, pf, fy0, fx0 + ix);
-        const double* s0 = sc + 3 * ixx + comp + (cz ? SP : 0);
-        for (int ry0 = 0; ry0 < nfy; ry0 += MG_R) {
-          double old[MG_R];
-          unsigned mk[MG_R];
+        // z pass of coarse row jy at x offsets 0 and +1 (the latter for odd columns)
+        auto zrow = [&](int jy, double& z0, double& z1) {
+          const double* q = col + jy * SW;
+          z0 = cz ? 0.5 * __dadd_rn(q[0], q[SP]) : q[0];
+          z1 = ox ? (cz ? 0.5 * __dadd_rn(q[3], q[SP + 3]) : q[3]) : 0.0;
+        };
+        double za0, za1;  // row jy (carried)
+        zrow(0, za0, za1);
+        for (int jy0 = 0; 2 * jy0 < nfy; jy0 += PR_B) {
+          double old[2 * PR_B];
+          unsigned mk[2 * PR_B];
 #pragma unroll
-          for (int k = 0; k < MG_R; ++k) {
-            if (ry0 + k >= nfy) break;
-            old[k] = ADD ? urow[(ry0 + k) * rowpitch] : 0.0;
-            mk[k] = mrow[(long long)(ry0 + k) * gf.mp];
+          for (int k = 0; k < 2 * PR_B; ++k) {
+            const int ry = 2 * jy0 + k;
+            if (ry >= nfy) break;
+            old[k] = ADD ? urow[ry * rowpitch] : 0.0;
+            mk[k] = mrow[(long long)ry * gf.mp];
           }
 #pragma unroll
-          for (int k = 0; k < MG_R; ++k) {
-            const int ry = ry0 + k;
-            if (ry >= nfy) break;
-            const int jy = ry >> 1, oy = ry & 1;
-            const double* q = s0 + jy * SW;
-            double y[2];
-#pragma unroll
-            for (int xx = 0; xx < 2; ++xx) {
-              if (xx && !ox) {
-                y[1] = 0.0;
-                continue;
-              }
-              // z pass (staged plane K+1 minus plane K is SP; z-odd rows average them)
-              double z0 = q[3 * xx], z1 = oy ? q[SW + 3 * xx] : 0.0;
-              if (cz) {
-                z0 = 0.5 * __dadd_rn(q[3 * xx - SP], z0);
-                if (oy) z1 = 0.5 * __dadd_rn(q[SW + 3 * xx - SP], z1);
-              }
-              y[xx] = oy ? 0.5 * __dadd_rn(z0, z1) : z0;  // y pass
-            }
-            double v = y[0];
-            if (ox) v = 0.5 * __dadd_rn(v, y[1]);  // x pass
-            if ((mk[k] >> comp) & 1u) v = 0.0;
-            urow[ry * rowpitch] = ADD ? __dadd_rn(old[k], v) : v;
+          for (int k = 0; k < PR_B; ++k) {
+            const int jy = jy0 + k;
+            if (2 * jy >= nfy) break;
+            // even fine row 2 jy: y = z(jy)
+            double v = ox ? 0.5 * __dadd_rn(za0, za1) : za0;
+            if ((mk[2 * k] >> comp) & 1u) v = 0.0;
+            urow[(2 * jy) * rowpitch] = ADD ? __dadd_rn(old[2 * k], v) : v;
+            if (2 * jy + 1 >= nfy) break;
+            // odd fine row 2 jy + 1: y = 0.5 (z(jy) + z(jy + 1))
+            double zb0, zb1;
+            zrow(jy + 1, zb0, zb1);
+            const double y0 = 0.5 * __dadd_rn(za0, zb0);
+            v = ox ? 0.5 * __dadd_rn(y0, 0.5 * __dadd_rn(za1, zb1)) : y0;
+            if ((mk[2 * k + 1] >> comp) & 1u) v = 0.0;
+            urow[(2 * jy + 1) * rowpitch] = ADD ? __dadd_rn(old[2 * k + 1], v) : v;
+            za0 = zb0;
+            za1 = zb1;
           }
         }
       }
@@ -383,13 +397,13 @@ __global__ void __launch_bounds__(MG_THREADS)
 }
 
 // one CTA per coarse (plane, row block, node block) unit covering the fine slab's owned planes
-static int prolong_grid(const ProlongBlk& b, int cap) {
+static int prolong_grid(const ProlongBlk& b, int cap) {  // (cap: CTAs)
   return fit_grid((long long)(b.K1 - b.K0) * b.nJb * b.nIb, 1, cap);
 }
 
 vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* uf,
                              const int* stop, cudaStream_t s) {
-  const ProlongBlk b = prolong_blocks(C->g, F->g);
+  const ProlongBlk b = prolong_blocks(C->g, F->g, F->nsm);
   launch_pdl(prolong_kernel<true>, prolong_grid(b, F->nsm * MG_CPS), MG_THREADS, prolong_smem(b), s, C->g,
              F->g, (const uint8_t*)F->mask, uc, uf, stop, b);
   count_launch();
@@ -399,7 +413,7 @@ vt_status launch_prolong_add(vt_grid* C, vt_grid* F, const double* uc, double* u
 
 vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
                              cudaStream_t s) {
-  const ProlongBlk b = prolong_blocks(C->g, F->g);
+  const ProlongBlk b = prolong_blocks(C->g, F->g, F->nsm);
   launch_pdl(prolong_kernel<false>, prolong_grid(b, F->nsm * MG_CPS), MG_THREADS, prolong_smem(b), s, C->g,
              F->g, (const uint8_t*)F->mask, uc, uf, stop, b);
   count_launch();
