@@ -293,7 +293,10 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
 // z -> y -> x pass order and rounding as the reference: bit-identical.  A
 // slab produces exactly the fine planes it owns.
 constexpr int PJ_MAX = 8, PI_MAX = 42;  // 6 PI <= 256 fine dofs per row: one per thread
-constexpr int PR_B = 3;                  // coarse rows (6 fine rows) per batch of read-modify-writes
+#ifndef VT_PR_B
+#define VT_PR_B 3
+#endif
+constexpr int PR_B = VT_PR_B;  // coarse rows (2 PR_B fine rows) per batch of read-modify-writes
 
 struct ProlongBlk {
   int K0, K1;            // coarse planes covering the fine slab's owned planes

@@ -351,7 +351,7 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
     for (cudaEvent_t& e : G->io_ev) VT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   int nch = nchunks < 1 ? 1 : nchunks;
-  if (nch > 16) nch = 16;
+  if (nch > 16) nch = 16;  // (io_ev holds 2 x 16 + 1 events)
   if (nch > nown) nch = nown;
   std::vector<int> pb(nch + 1);
   for (int c = 0; c <= nch; ++c) pb[c] = g.pA + (int)((long long)nown * c / nch);
@@ -364,13 +364,13 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
   VT_CUDA(cudaEventRecord(ev_done, s));
   VT_CUDA(cudaStreamWaitEvent(G->io_in, ev_done, 0));
   VT_CUDA(cudaStreamWaitEvent(G->io_out, ev_done, 0));
+  // the input copy stream carries copies only, so the H2D engine never waits
+  // for a kernel between chunks
   for (int c = 0; c < nch; ++c) {
     const size_t off = (size_t)(pb[c] - g.pA) * dplane;
     const size_t cnt = (size_t)(pb[c + 1] - pb[c]) * dplane;
     VT_CUDA(cudaMemcpyAsync(G->io_stage + off, hsrc + off, cnt * sizeof(double),
                             cudaMemcpyHostToDevice, G->io_in));
-    VT_TRY(launch_unpack_project(G, G->io_stage + off, pb[c], pb[c + 1], G->io_raw, G->io_proj,
-                                 G->io_in));
     VT_CUDA(cudaEventRecord(ev_in[c], G->io_in));
   }
   for (int c = 0; c < nch; ++c) {
@@ -380,6 +380,8 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
     const int ob = c == 0 ? pb[0] : pb[c] - 1;
     const int oe = c == nch - 1 ? pb[nch] : pb[c + 1] - 1;
     VT_CUDA(cudaStreamWaitEvent(s, ev_in[c], 0));
+    const size_t ioff = (size_t)(pb[c] - g.pA) * dplane;
+    VT_TRY(launch_unpack_project(G, G->io_stage + ioff, pb[c], pb[c + 1], G->io_raw, G->io_proj, s));
     if (oe > ob) {
       VT_TRY(launch_hex8(G, H8_APPLY, false, scale, G->io_proj, G->io_raw, nullptr, G->io_v, 0.0,
                          nullptr, nullptr, s, ob, oe));
@@ -397,6 +399,7 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
   VT_CUDA(cudaStreamSynchronize(s));
   return VT_OK;
 }
+
 
 vt_status vt_diagonal(vt_grid* G, const double* scale, double* d, void* stream) {
   return launch_diag(G, scale, d, (cudaStream_t)stream);
