@@ -14,6 +14,10 @@ namespace cg = cooperative_groups;
 namespace vt {
 
 constexpr int DS_THREADS = 256;
+#ifndef VT_OC_B
+#define VT_OC_B 1
+#endif
+constexpr int OC_B = VT_OC_B;  // OC bisection: elements in flight per thread
 
 __device__ __forceinline__ double corner_u(const Geom& g, const double* u, int i, int j, int k,
                                            int c, int comp) {
@@ -234,11 +238,26 @@ __global__ void oc_kernel(OcArgs a) {
   }
   auto mean_at = [&](double lam) {
     double s = 0.0;
-    for (long long e = t0; e < a.nel; e += stride) {
-      if (a.cls[e] != 0) continue;
-      const double x = a.x[e];
-      s += oc_cand(x, fmax(-a.dc[e], 0.0), a.dv[e], lam, a.eta, a.q, fmax(0.0, x - a.move),
-                   fmin(1.0, x + a.move));
+    // OC_B elements in flight per thread (same per-thread order as a plain
+    // grid-stride loop: the partial sums are unchanged)
+    for (long long e0 = t0; e0 < a.nel; e0 += OC_B * stride) {
+      double xv[OC_B], dcv[OC_B], dvv[OC_B];
+      bool act[OC_B];
+#pragma unroll
+      for (int k = 0; k < OC_B; ++k) {
+        const long long e = e0 + k * stride;
+        act[k] = e < a.nel && a.cls[e] == 0;
+        if (act[k]) {
+          xv[k] = a.x[e];
+          dcv[k] = a.dc[e];
+          dvv[k] = a.dv[e];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < OC_B; ++k)
+        if (act[k])
+          s += oc_cand(xv[k], fmax(-dcv[k], 0.0), dvv[k], lam, a.eta, a.q, fmax(0.0, xv[k] - a.move),
+                       fmin(1.0, xv[k] + a.move));
     }
     const double tot = grid_sum(grid, s, a.part, parity, red);
     parity ^= 1;
@@ -386,8 +405,9 @@ vt_status vt_oc_update(vt_grid* G, const double* rho, const int8_t* classes, con
     VT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oc_kernel, DS_THREADS, 0));
     max_blocks = per_sm * G->nsm;
   }
-  int grid = G->nsm * 2;
-  if (grid > max_blocks) grid = max_blocks;
+  // every resident block (one grid barrier per bisection step, so latency
+  // hiding matters more than the partial count)
+  int grid = max_blocks;
   if (grid > 2048) grid = 2048;
   OcArgs a;
   a.nel = G->nel_local();
