@@ -511,6 +511,98 @@ __global__ void __launch_bounds__(1024, 1)
   if (threadIdx.x == 0) *status = bad;
 }
 
+// Small coarsest systems (n^2 doubles fit in shared memory: n <= 160, e.g.
+// 135 dofs at cfg2/cfg3): assembly, Cholesky, in-place triangular inverse
+// and Kinv = L^-T L^-1 in ONE CTA entirely in shared memory -- the global-
+// memory version pays a memory round trip on every one of its ~3n dependent
+// steps (0.85 ms per refresh at cfg2).  Same assembly order and the same
+// right-looking Cholesky recurrence; the inverse follows LAPACK dtrti2
+// (lower, non-unit).  A0 (the assembled matrix) goes to global for the
+// refinement step of the coarse solve.
+constexpr int COARSE_SMEM_N = 160;
+__global__ void __launch_bounds__(1024, 1)
+    coarse_factor_smem_kernel(Geom g, const double* scale, const double* k0l, const double* mats,
+                              const uint8_t* mask, int n, double* A0, double* Kinv, int* status) {
+  griddep_wait();
+  extern __shared__ double As[];  // n x n, then n scratch
+  double* tmp = As + (size_t)n * n;
+  const int nx1 = g.nx + 1, ny1 = g.ny + 1;
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) As[t] = 0.0;
+  __syncthreads();
+  const int nel = g.nx * g.ny * g.nz;
+  for (int e = 0; e < nel; ++e) {
+    const int i = e % g.nx, j = (e / g.nx) % g.ny, k = e / (g.nx * g.ny);
+    const double sc = mats ? 0.0 : scale[elem_off(g, k + 1, j, i)];
+    for (int t = threadIdx.x; t < 576; t += blockDim.x) {
+      const int a = t / 24, b = t % 24;
+      const int ca = a / 3, cb = b / 3;
+      const int na = (i + (ca & 1)) + (j + ((ca >> 1) & 1)) * nx1 + (k + (ca >> 2)) * nx1 * ny1;
+      const int nb = (i + (cb & 1)) + (j + ((cb >> 1) & 1)) * nx1 + (k + (cb >> 2)) * nx1 * ny1;
+      As[(3 * na + a % 3) * n + 3 * nb + b % 3] += mats ? mats[(long long)e * 576 + t] : sc * k0l[t];
+    }
+    __syncthreads();
+  }
+  // identity rows / columns on fixed dofs
+  for (int d = threadIdx.x; d < n; d += blockDim.x) {
+    const int node = d / 3, c = d % 3;
+    const int i = node % nx1, j = (node / nx1) % ny1, k = node / (nx1 * ny1);
+    tmp[d] = ((mask[mask_off(g, k + 1, j, i)] >> c) & 1u) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+    const int r = t / n, c = t % n;
+    if (tmp[r] != 0.0 || tmp[c] != 0.0) As[t] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) A0[t] = As[t];
+  // right-looking Cholesky, lower triangle
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double d = As[j * n + j];
+    const double piv = (d > 0.0 && isfinite(d)) ? sqrt(d) : 1.0;
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (threadIdx.x == 0) bad = 1;
+    }
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) As[i * n + j] /= piv;
+    __syncthreads();
+    if (threadIdx.x == 0) As[j * n + j] = piv;
+    const int m = n - j - 1;
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+      const int ii = j + 1 + t / m, kk = j + 1 + t % m;
+      if (kk <= ii) As[ii * n + kk] -= As[ii * n + j] * As[kk * n + j];
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (threadIdx.x == 0) *status = 1;
+    return;
+  }
+  // in-place inverse of the lower-triangular factor (LAPACK dtrti2, 'L', 'N')
+  for (int j = n - 1; j >= 0; --j) {
+    const double ajj = -1.0 / As[j * n + j];
+    // tmp = T x with T the inverted trailing block, x = column j below the diagonal
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      double acc = 0.0;
+      for (int k = j + 1; k <= i; ++k) acc = fma(As[i * n + k], As[k * n + j], acc);
+      tmp[i] = acc;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) As[i * n + j] = ajj * tmp[i];
+    if (threadIdx.x == 0) As[j * n + j] = -ajj;
+    __syncthreads();
+  }
+  // Kinv = W^T W with W = L^-1 (lower): Kinv[i][j] = sum_{k >= max(i,j)} W[k][i] W[k][j]
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+    const int i = t / n, j = t % n;
+    double acc = 0.0;
+    for (int k = max(i, j); k < n; ++k) acc = fma(As[k * n + i], As[k * n + j], acc);
+    Kinv[t] = acc;
+  }
+  if (threadIdx.x == 0) *status = 0;
+}
+
 // W = L^{-1}: one thread per column
 __global__ void tri_inverse_kernel(int n, const double* A, double* W) {
   griddep_wait();
@@ -860,12 +952,25 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
                                    (int)(n * sizeof(double))));
     }
   }
-  launch_pdl(coarse_factor_kernel, 1, 1024, 0, s, C->g, H->scale[L - 1], H->k0l,
-                                          (H->scheme == 1 && L > 1) ? H->mats[L - 1] : nullptr,
-                                          C->mask, n, H->A, H->A0, H->status);
-  launch_pdl(tri_inverse_kernel, (n + 127) / 128, 128, 0, s, n, H->A, H->W);
-  launch_pdl(gram_kernel, C->nsm * 4, 256, 0, s, n, H->W, H->Kinv);
-  count_launch(3);
+  const double* cmats = (H->scheme == 1 && L > 1) ? H->mats[L - 1] : nullptr;
+  if (n <= COARSE_SMEM_N) {
+    const size_t sm = ((size_t)n * n + n) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      VT_CUDA(cudaFuncSetAttribute(coarse_factor_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(((size_t)COARSE_SMEM_N * COARSE_SMEM_N + COARSE_SMEM_N) * sizeof(double))));
+      attr = true;
+    }
+    launch_pdl(coarse_factor_smem_kernel, 1, 1024, sm, s, C->g, H->scale[L - 1], H->k0l, cmats,
+               C->mask, n, H->A0, H->Kinv, H->status);
+    count_launch(1);
+  } else {
+    launch_pdl(coarse_factor_kernel, 1, 1024, 0, s, C->g, H->scale[L - 1], H->k0l, cmats, C->mask, n,
+               H->A, H->A0, H->status);
+    launch_pdl(tri_inverse_kernel, (n + 127) / 128, 128, 0, s, n, H->A, H->W);
+    launch_pdl(gram_kernel, C->nsm * 4, 256, 0, s, n, H->W, H->Kinv);
+    count_launch(3);
+  }
   VT_CUDA(cudaGetLastError());
   int hb[2] = {0, 0};
   VT_CUDA(cudaMemcpyAsync(&hb[0], bad, sizeof(int), cudaMemcpyDeviceToHost, s));
