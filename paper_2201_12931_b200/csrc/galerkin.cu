@@ -130,6 +130,14 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
   griddep_wait();
   __shared__ double A[576], P[576];
   __shared__ double m[24];
+  // the octant tables in shared memory (threads of a warp index different
+  // columns: the constant cache would serialize them)
+  __shared__ double Ts[8 * 8 * 8];
+  // FROM_SCALE: the current child's 8 fine scales and correction ids, loaded
+  // once per child instead of once per matrix entry
+  __shared__ double s8[8];
+  __shared__ int c8[8];
+  for (int t = threadIdx.x; t < 512; t += blockDim.x) Ts[t] = (&c_T[0][0][0])[t];
   const long long nelc = (long long)cnx * cny * cnz;
   for (long long E = blockIdx.x; E < nelc; E += gridDim.x) {
     const int I = (int)(E % cnx), J = (int)((E / cnx) % cny), K = (int)(E / ((long long)cnx * cny));
@@ -143,19 +151,34 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
         const unsigned mk = mask[mask_off(gl, fk + ((corner >> 2) & 1) + 1, fj + ((corner >> 1) & 1),
                                           fi + (corner & 1))];
         m[threadIdx.x] = ((mk >> comp) & 1u) ? 0.0 : 1.0;
+      } else if (FROM_SCALE && threadIdx.x < 32) {
+        const int cc = threadIdx.x - 24;
+        s8[cc] = k1.scale[elem_off(k1.gf, 2 * fk + (cc >> 2) + 1, 2 * fj + ((cc >> 1) & 1), 2 * fi + (cc & 1))];
+        c8[cc] = k1.corr_of ? k1.corr_of[e * 8 + cc] : -1;
       }
       __syncthreads();
       for (int q = threadIdx.x; q < 576; q += blockDim.x) {
-        const double kq = FROM_SCALE ? k1_entry(k1, e, fi, fj, fk, q) : mats_l[e * 576 + q];
+        double kq;
+        if (FROM_SCALE) {  // k1_entry with the child's invariants hoisted (same order)
+          kq = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) kq = fma(s8[cc], k1.G[cc * 576 + q], kq);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc)
+            if (c8[cc] >= 0) kq = __dadd_rn(kq, __dmul_rn(s8[cc], k1.corr[(long long)c8[cc] * 576 + q]));
+        } else {
+          kq = mats_l[e * 576 + q];
+        }
         A[q] = kq * (m[q / 24] * m[q % 24]);
       }
       __syncthreads();
+      const double* Tc = Ts + c * 64;
       // P = A W_c: P[a][b] = sum_x A[a][3x + b%3] T_c[x][b/3]
       for (int q = threadIdx.x; q < 576; q += blockDim.x) {
         const int a = q / 24, b = q % 24;
         double s = 0.0;
 #pragma unroll
-        for (int x = 0; x < 8; ++x) s = fma(A[a * 24 + 3 * x + b % 3], c_T[c][x][b / 3], s);
+        for (int x = 0; x < 8; ++x) s = fma(A[a * 24 + 3 * x + b % 3], Tc[x * 8 + b / 3], s);
         P[q] = s;
       }
       __syncthreads();
@@ -166,7 +189,7 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
         const int a = q / 24, b = q % 24;
         double s = 0.0;
 #pragma unroll
-        for (int x = 0; x < 8; ++x) s = fma(c_T[c][x][a / 3], P[(3 * x + a % 3) * 24 + b], s);
+        for (int x = 0; x < 8; ++x) s = fma(Tc[x * 8 + a / 3], P[(3 * x + a % 3) * 24 + b], s);
         acc[r] = __dadd_rn(acc[r], s);
       }
     }
