@@ -187,6 +187,24 @@ vt_status vt_compliance(vt_grid *g, const double *f, const double *u, double *c,
  * element order [ref: optimize.py:195-213]; grav_coef = -uw*g*h^3/8 */
 vt_status vt_sensitivities(vt_grid *g, const double *u, const double *rho, double p, double kmin,
                            double E, int grav_axis, double grav_coef, double *dc, void *stream);
+/* Two-material SIMP (BASELINE cfg4; NO reference counterpart -- the
+ * reference's SPEC.md:15,178 lists multi-material as never developed, so this
+ * extends simp_scale / sensitivities [ref: element.py:102-118,
+ * optimize.py:195-213] and is pinned only through its single-material limit
+ * eB = 1 and finite differences).  Element modulus E s(rho) m(phi) with
+ * m = eB + (1 - eB) phi^p, eB = E_B / E_A in [0, 1].
+ * scale: vt element layout; rho_mg (optional, plain element order) =
+ * rho m^(1/p), the density the homogenized coarse levels average.
+ * VT_EDENSITY when rho or phi lies outside [0, 1]. */
+vt_status vt_scale_two_material(vt_grid *g, const double *rho, const double *phi, double p,
+                                double kmin, double E, double eB, double *scale, double *rho_mg,
+                                void *stream);
+/* dc_rho = -E s'(rho) m(phi) u_e'K0u_e (+ gravity term as vt_sensitivities),
+ * dc_phi = -E s(rho) p phi^(p-1) (1 - eB) u_e'K0u_e */
+vt_status vt_sensitivities_two_material(vt_grid *g, const double *u, const double *rho,
+                                        const double *phi, double p, double kmin, double E,
+                                        double eB, int grav_axis, double grav_coef, double *dc_rho,
+                                        double *dc_phi, void *stream);
 /* f = scatter(rho_e g_unit) (+ f_ext) (zero on fixed if zero_fixed)
  * [ref: optimize.py:216-231] */
 vt_status vt_gravity_load(vt_grid *g, const double *rho, int grav_axis, double grav_coef,

@@ -50,6 +50,13 @@ from .design import (
     sensitivities,
     update_gravity_load,
 )
+from .multimaterial import (
+    TwoMaterialRecord,
+    TwoMaterialResult,
+    initial_phases,
+    run_two_material,
+    sensitivities_two_material,
+)
 
 __version__ = "0.1.0"
 

@@ -77,6 +77,8 @@ _SIGS = {
     "vt_compliance": (I, [P, P, P, C.POINTER(D), P]),
     "vt_sensitivities": (I, [P, P, P, D, D, D, I, D, P, P]),
     "vt_gravity_load": (I, [P, P, I, D, P, I, P, P]),
+    "vt_scale_two_material": (I, [P, P, P, D, D, D, D, P, P, P]),
+    "vt_sensitivities_two_material": (I, [P, P, P, P, D, D, D, D, I, D, P, P, P]),
     "vt_filter_create": (I, [C.POINTER(P), P, I, P]),
     "vt_filter_destroy": (I, [P]),
     "vt_filter_wsum": (P, [P]),

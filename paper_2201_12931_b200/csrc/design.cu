@@ -27,10 +27,16 @@ __device__ __forceinline__ double corner_u(const Geom& g, const double* u, int i
 
 // dc_e = -(E p rho^(p-1) (1-kmin)) * u_e'K0u_e  (+ 2 u_e.g_unit)
 // u_e'K0u_e = sum over the 21 coefficient pairs C.O of the factorized form.
+// TWO: two-material SIMP (no reference counterpart): the
+// element modulus is E s(rho) m(phi), m = eB + (1 - eB) phi^p, and the kernel
+// also writes dc_phi = -E s(rho) p phi^(p-1) (1 - eB) u_e'K0u_e.
+template <bool TWO>
 __global__ void sens_kernel(Geom g, const double* __restrict__ u, const double* __restrict__ rho,
                             double p, double kmin, double E, int gax, double gcoef,
                             const double kc0, const double kc1, const double kc2, const double kc3,
-                            const double kc4, const double kc5, double* __restrict__ dc) {
+                            const double kc4, const double kc5, double* __restrict__ dc,
+                            const double* __restrict__ phi, double eB,
+                            double* __restrict__ dcphi) {
   const long long nel = (long long)g.nx * g.ny * (g.k1 - g.k0);
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
        e += (long long)gridDim.x * blockDim.x) {
@@ -101,10 +107,43 @@ __global__ void sens_kernel(Geom g, const double* __restrict__ u, const double* 
     else if (pm1 == 0.0) rp = 1.0;
     else if (pm1 == 0.5) rp = sqrt(x);
     else rp = pow(x, pm1);
-    const double ds = __dmul_rn(E, __dmul_rn(__dmul_rn(p, rp), 1.0 - kmin));
+    double ds = __dmul_rn(E, __dmul_rn(__dmul_rn(p, rp), 1.0 - kmin));
+    if (TWO) {
+      const double y = phi[e];
+      const double m = __dadd_rn(eB, __dmul_rn(1.0 - eB, simp_pow(y, p)));
+      ds = __dmul_rn(ds, m);
+      // E * s(rho) * (p * phi^(p-1) * (1 - eB))
+      const double s = __dmul_rn(E, __dadd_rn(kmin, __dmul_rn(simp_pow(x, p), 1.0 - kmin)));
+      const double dm = __dmul_rn(__dmul_rn(p, simp_pow(y, pm1)), 1.0 - eB);
+      dcphi[e] = __dmul_rn(-__dmul_rn(s, dm), quad);
+    }
     double out = __dmul_rn(-ds, quad);
     if (gax >= 0) out += 2.0 * (gcoef * C[gax][0]);
     dc[e] = out;
+  }
+}
+
+// Two-material element scale (vt element layout) and the density the
+// homogenized coarse levels average: rho_mg = rho m(phi)^(1/p), so that
+// s(rho_mg) ~ s(rho) m(phi) up to kmin (preconditioner only; the fine operator
+// uses the exact scale).
+__global__ void two_scale_kernel(Geom g, const double* __restrict__ rho,
+                                 const double* __restrict__ phi, double p, double kmin, double E,
+                                 double eB, double* __restrict__ scale, double* __restrict__ rho_mg,
+                                 int* bad) {
+  const long long nel = (long long)g.nx * g.ny * (g.k1 - g.k0);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % g.nx);
+    const long long r = e / g.nx;
+    const int j = (int)(r % g.ny);
+    const int q = (int)(r / g.ny) + 1;
+    const double x = rho[e], y = phi[e];
+    if (!(x >= 0.0 && x <= 1.0 && y >= 0.0 && y <= 1.0)) *bad = 1;
+    const double m = __dadd_rn(eB, __dmul_rn(1.0 - eB, simp_pow(y, p)));
+    const double s = __dmul_rn(E, __dadd_rn(kmin, __dmul_rn(simp_pow(x, p), 1.0 - kmin)));
+    scale[elem_off(g, q, j, i)] = __dmul_rn(s, m);
+    if (rho_mg) rho_mg[e] = fmin(1.0, x * pow(m, 1.0 / p));
   }
 }
 
@@ -327,10 +366,44 @@ vt_status vt_sensitivities(vt_grid* G, const double* u, const double* rho, doubl
                            double E, int grav_axis, double grav_coef, double* dc, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const double* k = G->coef.kc;
-  sens_kernel<<<G->nsm * 8, DS_THREADS, 0, s>>>(G->g, u, rho, p, kmin, E, grav_axis, grav_coef,
-                                                k[0], k[1], k[2], k[3], k[4], k[5], dc);
+  sens_kernel<false><<<G->nsm * 8, DS_THREADS, 0, s>>>(G->g, u, rho, p, kmin, E, grav_axis, grav_coef,
+                                                       k[0], k[1], k[2], k[3], k[4], k[5], dc,
+                                                       nullptr, 1.0, nullptr);
   count_launch();
   VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status vt_sensitivities_two_material(vt_grid* G, const double* u, const double* rho,
+                                        const double* phi, double p, double kmin, double E,
+                                        double eB, int grav_axis, double grav_coef, double* dc_rho,
+                                        double* dc_phi, void* stream) {
+  if (!(eB >= 0.0 && eB <= 1.0)) return fail(VT_EINVAL, "modulus ratio must lie in [0, 1]");
+  cudaStream_t s = (cudaStream_t)stream;
+  const double* k = G->coef.kc;
+  sens_kernel<true><<<G->nsm * 8, DS_THREADS, 0, s>>>(G->g, u, rho, p, kmin, E, grav_axis, grav_coef,
+                                                      k[0], k[1], k[2], k[3], k[4], k[5], dc_rho,
+                                                      phi, eB, dc_phi);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status vt_scale_two_material(vt_grid* G, const double* rho, const double* phi, double p,
+                                double kmin, double E, double eB, double* scale, double* rho_mg,
+                                void* stream) {
+  if (!(eB >= 0.0 && eB <= 1.0)) return fail(VT_EINVAL, "modulus ratio must lie in [0, 1]");
+  cudaStream_t s = (cudaStream_t)stream;
+  int* bad = reinterpret_cast<int*>(G->scalars + 1);
+  VT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  two_scale_kernel<<<G->nsm * 8, DS_THREADS, 0, s>>>(G->g, rho, phi, p, kmin, E, eB, scale, rho_mg,
+                                                     bad);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  int hb = 0;
+  VT_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  VT_CUDA(cudaStreamSynchronize(s));
+  if (hb) return fail(VT_EDENSITY, "density or phase fraction outside [0, 1]");
   return VT_OK;
 }
 

@@ -39,18 +39,6 @@ __device__ __forceinline__ long long owned_nodes(const Geom& g) {
 }
 
 // ---------------------------------------------------------------- SIMP scale
-__device__ __forceinline__ double simp_pow(double r, double p) {
-  if (p == 3.0) {  // correctly rounded r^3 (numpy's pow agrees in ~95% of cases, else 1 ulp)
-    const double hi = r * r;
-    const double lo = fma(r, r, -hi);
-    return fma(hi, r, lo * r);
-  }
-  if (p == 2.0) return r * r;
-  if (p == 1.0) return r;
-  if (p == 0.5) return sqrt(r);
-  if (p == 0.0) return 1.0;
-  return pow(r, p);
-}
 
 __global__ void scale_kernel(Geom g, const double* rho, double p, double kmin, double E,
                              double* scale, int* bad) {

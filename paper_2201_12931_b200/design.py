@@ -339,8 +339,12 @@ class DeviceRun:
         st = OperatorState.__new__(OperatorState)
         st.grid, st.model, st.stiffness = self.problem.grid, model, self.k0
         st.fixed_mask, st.fixed_idx = self.fixed_mask, np.flatnonzero(self.fixed_mask)
-        st.dgrid, st.rho_dev, st.scale_dev, st.densities = self.d, self.rho, self.scale, None
+        st.dgrid, st.rho_dev, st.scale_dev, st.densities = self.d, self.mg_rho(), self.scale, None
         return st
+
+    def mg_rho(self) -> torch.Tensor:
+        """Densities the homogenized coarse levels average (the design densities)."""
+        return self.rho
 
     def solve(self, model):
         """refresh + MGPCG for the current densities; returns SolveReport."""
@@ -356,7 +360,7 @@ class DeviceRun:
                 self.hier = build_hierarchy(self.problem.grid, self.state_view(model), self.max_levels,
                                             scheme=self.scheme, omega=self.omega)
             else:
-                self.hier._refresh_raw(self.rho, self.scale, model)
+                self.hier._refresh_raw(self.mg_rho(), self.scale, model)
             aux = 4 * d.n_dofs + self.hier.vector_scalars
             if aux > AUX_BUDGET_FACTOR * d.n_dofs:
                 raise SolverBreakdown(f"auxiliary vector budget {aux} exceeds {AUX_BUDGET_FACTOR} * n")

@@ -23,7 +23,12 @@ from paper_2201_12931_b200._lib import lib  # noqa: E402
 from paper_2201_12931_b200.design import DeviceRun  # noqa: E402
 from paper_2201_12931_b200.device import ptr, stream_ptr  # noqa: E402
 
-HBM = 6650.0  # B200_PROFILING.md fallback peak (GB/s)
+try:  # driver-measured copy bandwidth of this pool's B200s, else the B200_PROFILING.md fallback
+    with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "MEASURED_PEAKS.json")) as _fh:
+        HBM = float(json.load(_fh)["hbm_gbs"])
+except (OSError, KeyError, ValueError):
+    HBM = 6650.0
 
 
 def measure(name):
@@ -67,12 +72,43 @@ def measure(name):
             "ms_per_cg_iter": 1e3 * sum(secs) / max(1, sum(its))}
 
 
+def measure_two_material(name, phase_frac=0.5, e_ratio=0.5, scheme="galerkin"):
+    """BASELINE cfg4's two-material SIMP (paper_2201_12931_b200.multimaterial):
+    two timed SIMP iterations (iterations 2-3) with both design fields updated."""
+    from paper_2201_12931_b200.multimaterial import TwoMaterialRun
+    c = cases.CONFIGS[name]
+    prob = c["builder"](*c["dims"])
+    g = prob.grid
+    opt = vb.OptConfig(volfrac=c["volfrac"], filter_radius=1.5 * g.h, ch_tol=1e-12)
+    R = TwoMaterialRun(prob, opt, phase_frac, e_ratio, vb.SolverConfig(tolerance=1e-5), scheme,
+                       c["levels"], 0.4)
+    R.solve(prob.model)
+    R.design_step(prob.model)
+    its, secs, comp = [], [], []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        ts = time.perf_counter()
+        rep = R.solve(prob.model)
+        cc, ch, vol, pvol = R.design_step(prob.model)
+        torch.cuda.synchronize()
+        secs.append(time.perf_counter() - ts)
+        its.append(rep.iterations)
+        comp.append(cc)
+    return {"dims": list(c["dims"]), "levels": c["levels"], "dofs": g.n_dofs, "elements": g.n_elements,
+            "builder": c["builder"].__name__, "scheme": scheme, "phase_frac": phase_frac,
+            "e_ratio": e_ratio, "simp_iter_s": sum(secs) / len(secs), "cg_iters": its,
+            "compliance": comp, "ms_per_cg_iter": 1e3 * sum(secs) / max(1, sum(its))}
+
+
 if __name__ == "__main__":
     names = sys.argv[1:] or ["cfg2", "cfg3", "cfg4"]
     out = {"gpu": torch.cuda.get_device_name(0), "peak_gbs": HBM,
            "note": "1 GPU; SIMP iterations 2-3 (refresh + homogenized MGPCG tol 1e-5 + design step), "
                    "device resident; apply = vt_apply_projected, 10 launches"}
     for n in names:
-        out[n] = measure(n)
+        if n.endswith("_two_material"):
+            out[n] = measure_two_material(n[: -len("_two_material")])
+        else:
+            out[n] = measure(n)
         torch.cuda.empty_cache()
     print(json.dumps(out))
