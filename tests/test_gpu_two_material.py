@@ -92,3 +92,19 @@ def test_two_material_unit_ratio_is_run():
     assert [r.cg_iters for r in a.records] == [r.cg_iters for r in b.records]
     assert np.array_equal(a.densities.values, b.densities.values)
     assert np.all(b.phases.values == 0.5)
+
+
+def test_two_material_self_weight_matches_oracle():
+    """BASELINE cfg4's combination (self-weight load + two materials) at small
+    size: the gravity term acts on rho only; tight solves on both sides."""
+    case, grid, prob = _cantilever(16, 8, 8, gravity=(2, 1.0, 1e-3))
+    its = 6
+    opt = vb.OptConfig(volfrac=0.3, filter_radius=1.5 * grid.h, max_iterations=its, ch_tol=1e-12)
+    res = vb.run_two_material(prob, opt, 0.5, e_ratio=0.5,
+                              solver=vb.SolverConfig(tolerance=1e-10, max_iterations=1000), max_levels=3)
+    rho, phi, u, recs = O.run_design_two_material(case, 0.3, 0.5, 0.5, 1.5 * case.h, its, tol=1e-10,
+                                                  maxit=1000, max_levels=3, ch_tol=1e-12)
+    worst = max(abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(res.records, recs))
+    assert worst <= 1e-6
+    assert np.abs(res.densities.values - rho).max() <= 1e-4
+    assert np.abs(res.phases.values - phi).max() <= 1e-4
