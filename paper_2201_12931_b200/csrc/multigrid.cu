@@ -12,6 +12,8 @@
 
 #include <vector>
 
+#include <atomic>
+
 #include "vt_internal.h"
 #include "vt_pcg.cuh"
 
@@ -799,7 +801,9 @@ vt_status vt_hier_create_ex(vt_hier** out, vt_grid* fine, int n_levels, double o
   if (fine->g.k0 != 0 || fine->g.k1 != fine->g.nz)
     return fail(VT_EINVAL, "multi-slab hierarchies are built by the distributed runtime");
   VT_CUDA(cudaSetDevice(fine->device));
+  static std::atomic<unsigned long long> next_uid{1};
   vt_hier* H = new vt_hier();
+  H->uid = next_uid++;
   H->omega = omega;
   H->sweeps = sweeps;
   H->lv.push_back(fine);

@@ -591,8 +591,12 @@ vt_status vt_pcg(vt_grid* G, const double* scale, int precond, vt_hier* H, const
   c0.skip_cand = 1;
   c0.skip_swap = 1;
   VT_CUDA(cudaMemcpyAsync(G->pcg_ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
-  // (re)capture the iteration graph when the operator / preconditioner changed
-  const void* key[4] = {scale, H, (const void*)(intptr_t)(precond + 1), G};
+  // (re)capture the iteration graph when the operator / preconditioner changed.
+  // The hierarchy is keyed by its unique id, not its address: a destroyed
+  // hierarchy's address (and its scale buffer's) can come back for a new one
+  // whose device buffers differ -- a stale graph would read freed memory.
+  const void* key[4] = {scale, (const void*)(uintptr_t)(H ? H->uid : 0),
+                        (const void*)(intptr_t)(precond + 1), G};
   if (!G->pcg_graph || memcmp(key, G->pcg_key, sizeof(key)) != 0) {
     VT_CUDA(cudaStreamSynchronize(s));
     VT_TRY(pcg_capture(G, scale, precond, H, s, &G->pcg_nodes));

@@ -122,6 +122,7 @@ struct vt_grid {
 
 // ------------------------------------------------------------------- hierarchy
 struct vt_hier {
+  unsigned long long uid = 0;      // unique per hierarchy (graph cache key: addresses get reused)
   std::vector<vt_grid*> lv;        // lv[0] = caller's fine grid (not owned)
   std::vector<double*> u, u2, r, f, scale, rho;
   double omega = 0.4;

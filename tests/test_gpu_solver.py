@@ -270,3 +270,33 @@ def test_cfg1_trajectory_parity():
           f"rho40 {np.abs(seen[40] - g['rho40']).max():.2e}")
     _traj_check(res, want, g["rho40"])
     assert np.abs(seen[20] - g["rho20"]).max() <= 1e-4
+
+
+def test_pcg_graph_not_reused_across_hierarchies():
+    """The per-grid PCG iteration graph is keyed by the hierarchy's identity, not
+    its address: a hierarchy destroyed and rebuilt (often at the same address,
+    with different device buffers and level count) must trigger a recapture."""
+    import gc
+
+    case, grid, prob = _cantilever(16, 8, 8)
+    rng = np.random.default_rng(11)
+    rho = rng.uniform(0.05, 1.0, grid.n_elements)
+    st = vb.OperatorState(grid, rho, vb.MaterialModel(), case.fixed_mask)
+    f = case.f_ext.copy()
+    f[case.fixed_mask] = 0.0
+    cfg = vb.SolverConfig(tolerance=1e-8, max_iterations=300)
+    k0 = O.hex8_k0(0.3, case.h)
+    scale = O.simp(rho, 3.0, 1e-9)
+    fixed = np.flatnonzero(case.fixed_mask)
+    for levels in (2, 3, 2, 3):
+        H = vb.build_hierarchy(grid, st, levels, scheme="homogenized")
+        x, rep = vb.mgcg_solve(st, H, f, cfg=cfg)
+        OH = O.hier_build(case.es, case.h, case.fixed_mask, levels)
+        O.hier_refresh(OH, rho, scale, k0, 3.0, 1e-9, 1.0)
+        xo, ro = O.pcg(lambda p: O.apply_k(p, case.es, fixed, k0, scale),
+                       lambda p, ff: O.resid_k(p, ff, case.es, fixed, k0, scale),
+                       lambda r: O.vcycle(OH, r), f, None, fixed, 1e-8, 300)
+        assert rep.iterations == ro.iterations, (levels, rep.iterations, ro.iterations)
+        assert rel_err(x, xo) <= 1e-7
+        del H
+        gc.collect()
