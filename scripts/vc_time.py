@@ -24,4 +24,6 @@ for _ in range(50):
     lib.vt_hier_vcycle(H._h, ptr(f), ptr(z), stream_ptr())
 e1.record()
 torch.cuda.synchronize()
-print(os.environ.get("VT_LIB_PATH", "default"), f"vcycle {e0.elapsed_time(e1) / 50 * 1e3:.1f} us")
+import hashlib
+zh = hashlib.sha1(d.download(z).tobytes()).hexdigest()[:12]
+print(os.environ.get("VT_LIB_PATH", "default"), f"vcycle {e0.elapsed_time(e1) / 50 * 1e3:.1f} us z-hash {zh}")
