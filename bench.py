@@ -63,7 +63,8 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region (NVML every
+    ~0.2 ms when pynvml is importable, else nvidia-smi)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -86,9 +87,49 @@ class ClockSampler:
                 pass
             self._stop.wait(0.2)
 
+    def _nvml_handle(self):
+        """NVML handle of the CUDA device `index` (matched by PCI id), or None."""
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return None
+
+    def _run_nvml(self, nv, h):
+        # NVML reads take microseconds: sample every ~0.2 ms so even a short
+        # timed region gets several readings (nvidia-smi takes ~50 ms per call)
+        bits = [(nv.nvmlClocksEventReasonHwSlowdown, 2), (nv.nvmlClocksEventReasonHwThermalSlowdown, 3),
+                (nv.nvmlClocksEventReasonSwThermalSlowdown, 4), (nv.nvmlClocksEventReasonSwPowerCap, 5)]
+        reasons_fn = (getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None)
+                      or getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons"))
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = reasons_fn(h)
+                row = [str(sm), str(mx), "", "", "", ""]
+                for b, i in bits:
+                    row[i] = "Active" if rs & b else "Not Active"
+                self.samples.append(row)
+            except Exception as e:  # noqa: BLE001 (reported in the summary)
+                self.err = repr(e)
+            self._stop.wait(0.0002)
+
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        nv = self._nvml_handle()
+        self.source = "nvml" if nv else "nvidia-smi"
+        target = (lambda: self._run_nvml(*nv)) if nv else self._run
+        self._t = threading.Thread(target=target, daemon=True)
         self._t.start()
+        # the first reading lands before the region starts (GPU already warm)
+        t0 = time.perf_counter()
+        while not self.samples and time.perf_counter() - t0 < (0.5 if nv else 5.0):
+            time.sleep(1e-4)
         return self
 
     def __exit__(self, *a):
@@ -97,13 +138,14 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "source": getattr(self, "source", None), "error": getattr(self, "err", None)}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples), "source": getattr(self, "source", None)}
 
 
 # ---------------------------------------------------------------------- ours
@@ -117,7 +159,10 @@ def _timed(fn, steps, stream):
     for _ in range(steps):
         fn()
     e1.record(stream)
-    e1.synchronize()
+    # poll instead of a blocking synchronize so the clock sampler thread gets
+    # the GIL while the region runs (device-timed: polling does not change it)
+    while not e1.query():
+        time.sleep(5e-5)
     return e0.elapsed_time(e1) * 1e-3 / steps
 
 
