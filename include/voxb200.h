@@ -224,6 +224,11 @@ vt_status vt_filter_correlate(vt_filter *F, const double *field, double *out, vo
 vt_status vt_oc_update(vt_grid *g, const double *rho, const int8_t *classes, const double *dc,
                        const double *dv, double volfrac, double move, double eta, double q,
                        double *rho_out, double *lam, int *steps, void *stream);
+/* The same OC update on plain (nel,) device arrays with no grid handle (the
+ * public oc_update of a bare density field) [ref: optimize.py:245-302]. */
+vt_status vt_oc_update_flat(long long nel, const double *rho, const int8_t *classes, const double *dc,
+                            const double *dv, double volfrac, double move, double eta, double q,
+                            double *rho_out, double *lam, int *steps, void *stream);
 /* max |a-b| and mean of a over active elements (blocking helpers of run()) */
 vt_status vt_change_volume(vt_grid *g, const double *a, const double *b, const int8_t *classes,
                            double *max_abs_diff, double *active_mean, void *stream);

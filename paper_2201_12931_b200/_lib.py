@@ -85,6 +85,7 @@ _SIGS = {
     "vt_filter_apply": (I, [P, P, P, D, P, P]),
     "vt_filter_correlate": (I, [P, P, P, P]),
     "vt_oc_update": (I, [P, P, P, P, P, D, D, D, D, P, C.POINTER(D), C.POINTER(I), P]),
+    "vt_oc_update_flat": (I, [I64, P, P, P, P, D, D, D, D, P, C.POINTER(D), C.POINTER(I), P]),
     "vt_change_volume": (I, [P, P, P, P, C.POINTER(D), C.POINTER(D), P]),
     "vt_nccl_id_bytes": (I, []),
     "vt_nccl_unique_id": (I, [P, I]),

@@ -360,6 +360,53 @@ struct vt_filter {
 
 using namespace vt;
 
+namespace vt {
+// whole OC bisection in one cooperative launch [ref: optimize.py:245-302];
+// part: 2 x (resident blocks, <= 2048) doubles, res: 6 doubles
+static vt_status oc_run(long long nel, int nsm, double* part, double* res_dev, const double* rho,
+                        const int8_t* classes, const double* dc, const double* dv, double volfrac,
+                        double move, double eta, double q, double* rho_out, double* lam, int* steps,
+                        cudaStream_t s) {
+  static int per_sm = 0;
+  if (!per_sm) VT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oc_kernel, DS_THREADS, 0));
+  // every resident block (one grid barrier per bisection step, so latency
+  // hiding matters more than the partial count)
+  int grid = per_sm * nsm;
+  if (grid > 2048) grid = 2048;
+  OcArgs a;
+  a.nel = nel;
+  a.x = rho;
+  a.cls = classes;
+  a.dc = dc;
+  a.dv = dv;
+  a.volfrac = volfrac;
+  a.move = move;
+  a.eta = eta;
+  a.q = q;
+  a.out = rho_out;
+  a.part = part;
+  a.res = res_dev;
+  void* args[] = {&a};
+  VT_CUDA(cudaLaunchCooperativeKernel((void*)oc_kernel, grid, DS_THREADS, args, 0, s));
+  count_launch();
+  double res[6];
+  VT_CUDA(cudaMemcpyAsync(res, a.res, sizeof(res), cudaMemcpyDeviceToHost, s));
+  VT_CUDA(cudaStreamSynchronize(s));
+  if (res[2] == 1.0) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "volume target unreachable within the move limits (reachable [%.6f, %.6f], target %g)",
+             res[4], res[5], volfrac);
+    return fail(VT_EVOLUME, buf);
+  }
+  if (res[2] == 2.0)
+    return fail(VT_EVOLUME, "bisection failed to reach the volume target after 200 halvings");
+  if (lam) *lam = res[0];
+  if (steps) *steps = (int)res[1];
+  return VT_OK;
+}
+}  // namespace vt
+
 extern "C" {
 
 vt_status vt_sensitivities(vt_grid* G, const double* u, const double* rho, double p, double kmin,
@@ -471,48 +518,23 @@ vt_status vt_filter_correlate(vt_filter* F, const double* field, double* out, vo
 vt_status vt_oc_update(vt_grid* G, const double* rho, const int8_t* classes, const double* dc,
                        const double* dv, double volfrac, double move, double eta, double q,
                        double* rho_out, double* lam, int* steps, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int per_sm = 0;
-    VT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, oc_kernel, DS_THREADS, 0));
-    max_blocks = per_sm * G->nsm;
-  }
-  // every resident block (one grid barrier per bisection step, so latency
-  // hiding matters more than the partial count)
-  int grid = max_blocks;
-  if (grid > 2048) grid = 2048;
-  OcArgs a;
-  a.nel = G->nel_local();
-  a.x = rho;
-  a.cls = classes;
-  a.dc = dc;
-  a.dv = dv;
-  a.volfrac = volfrac;
-  a.move = move;
-  a.eta = eta;
-  a.q = q;
-  a.out = rho_out;
-  a.part = G->partial;
-  a.res = G->scalars + 8;
-  void* args[] = {&a};
-  VT_CUDA(cudaLaunchCooperativeKernel((void*)oc_kernel, grid, DS_THREADS, args, 0, s));
-  count_launch();
-  double res[6];
-  VT_CUDA(cudaMemcpyAsync(res, a.res, sizeof(res), cudaMemcpyDeviceToHost, s));
-  VT_CUDA(cudaStreamSynchronize(s));
-  if (res[2] == 1.0) {
-    char buf[256];
-    snprintf(buf, sizeof(buf),
-             "volume target unreachable within the move limits (reachable [%.6f, %.6f], target %g)",
-             res[4], res[5], volfrac);
-    return fail(VT_EVOLUME, buf);
-  }
-  if (res[2] == 2.0)
-    return fail(VT_EVOLUME, "bisection failed to reach the volume target after 200 halvings");
-  if (lam) *lam = res[0];
-  if (steps) *steps = (int)res[1];
-  return VT_OK;
+  return vt::oc_run(G->nel_local(), G->nsm, G->partial, G->scalars + 8, rho, classes, dc, dv, volfrac,
+                    move, eta, q, rho_out, lam, steps, (cudaStream_t)stream);
+}
+
+vt_status vt_oc_update_flat(long long nel, const double* rho, const int8_t* classes, const double* dc,
+                            const double* dv, double volfrac, double move, double eta, double q,
+                            double* rho_out, double* lam, int* steps, void* stream) {
+  if (nel <= 0) return fail(VT_EINVAL, "element count must be positive");
+  // per-device scratch: 2 x 2048 block partials + the result words
+  static double* scratch[64] = {};
+  int dev = 0, nsm = 0;
+  VT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(VT_EINVAL, "device ordinal out of range");
+  VT_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (!scratch[dev]) VT_CUDA(cudaMalloc(&scratch[dev], (2 * 2048 + 16) * sizeof(double)));
+  return vt::oc_run(nel, nsm, scratch[dev], scratch[dev] + 2 * 2048, rho, classes, dc, dv, volfrac,
+                    move, eta, q, rho_out, lam, steps, (cudaStream_t)stream);
 }
 
 vt_status vt_change_volume(vt_grid* G, const double* a, const double* b, const int8_t* classes,

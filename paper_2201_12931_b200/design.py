@@ -250,12 +250,17 @@ def oc_update(rho: DensityField, dc, dv, cfg: OptConfig) -> OcResult:
     dva = np.asarray(dv, dtype=np.float64)
     if np.any(dva[rho.regions.active] <= 0):
         raise ValueError("volume gradient must be positive")
-    # the kernel only needs a flat element count: use an (nel, 1, 1) grid
-    d = device_grid(StructuredGrid(nel, 1, 1, 1.0), 0.3, None)
-    rt = d.plain(rho.values)
-    ct = torch.as_tensor(np.ascontiguousarray(rho.regions.classes, dtype=np.int8), device=rt.device)
+    require_cuda()
+    dev = f"cuda:{torch.cuda.current_device()}"
+    flat = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+    rt = flat(rho.values)
+    ct = torch.as_tensor(np.ascontiguousarray(rho.regions.classes, dtype=np.int8), device=dev)
     out = torch.empty_like(rt)
-    lam, steps = _oc_device(d, rt, ct, d.plain(dc), d.plain(dva), cfg, out)
+    lam, steps = C.c_double(), C.c_int()
+    check(lib.vt_oc_update_flat(nel, ptr(rt), ptr(ct), ptr(flat(dc)), ptr(flat(dva)), float(cfg.volfrac),
+                                float(cfg.move), float(cfg.eta), float(cfg.q), ptr(out), C.byref(lam),
+                                C.byref(steps), stream_ptr()))
+    lam, steps = lam.value, steps.value
     return OcResult(DensityField(out.cpu().numpy(), rho.regions), lam, steps)
 
 

@@ -258,7 +258,7 @@ class SlabRun:
 
     def __init__(self, problem, opt, solver: SolverConfig, max_levels=None, omega: float = 0.4,
                  nranks: int = 1, rank: int = 0, nlocal: Optional[int] = None, nccl_id: Optional[bytes] = None,
-                 init_densities=None, group=None):
+                 init_densities=None, group=None, init_displacement=None):
         from .design import filter_weights, initial_densities
 
         if solver.preconditioner != "multigrid":
@@ -285,13 +285,22 @@ class SlabRun:
         self.dv = [torch.ones_like(r) for r in self.rho]
         self.dc = [torch.empty_like(r) for r in self.rho]
         self.dcf = [torch.empty_like(r) for r in self.rho]
-        self.u = S.zeros()
+        # a resumed run warm-starts its first solve from the stored displacement,
+        # as the reference's run() does (optimize.py:344-360)
+        if init_displacement is not None:
+            u0 = np.array(init_displacement, dtype=np.float64)
+            if u0.shape != (grid.n_dofs,):
+                raise ValueError(f"initial displacement must have length {grid.n_dofs}")
+            u0[fm] = 0.0
+            self.u = S.upload(u0)
+        else:
+            self.u = S.zeros()
         R, kern = filter_weights(grid.h, opt.filter_radius)
         check(lib.vt_dist_filter_create(S._h, R, kern.ctypes.data_as(C.c_void_p)), "vt_dist_filter_create")
 
     @classmethod
     def from_process_group(cls, problem, opt, solver, max_levels=None, omega=0.4, init_densities=None,
-                           group=None):
+                           group=None, init_displacement=None):
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -303,7 +312,8 @@ class SlabRun:
             obj[0] = bytes(buf)
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls(problem, opt, solver, max_levels, omega, nranks=world, rank=rank, nlocal=1,
-                   nccl_id=obj[0], init_densities=init_densities, group=group)
+                   nccl_id=obj[0], init_densities=init_densities, group=group,
+                   init_displacement=init_displacement)
 
     def solve(self, model) -> SolveReport:
         S = self.S
@@ -362,14 +372,18 @@ class SlabRun:
         if self.S.nlocal != self.S.nranks:
             import torch.distributed as dist
 
-            t = torch.from_numpy(np.array(out))
-            dist.all_reduce(t, group=self.group)  # disjoint owned planes: the sum assembles the field
-            out = t.numpy()
+            # disjoint owned planes: the sum assembles the field.  NCCL groups
+            # reduce device tensors only; gloo takes host tensors
+            dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+            t = torch.from_numpy(np.array(out)).to(dev)
+            dist.all_reduce(t, group=self.group)
+            out = t.cpu().numpy()
         return out
 
 
 def run_slabs(problem, opt, solver: SolverConfig = SolverConfig(), max_levels=None, omega: float = 0.4,
-              nranks: int = 1, group=None, init_densities=None, start_iteration: int = 0, on_iteration=None):
+              nranks: int = 1, group=None, init_densities=None, start_iteration: int = 0, on_iteration=None,
+              init_displacement=None):
     """run() (optimize.py:323-455, homogenized scheme) on z-slabs: all `nranks`
     slabs in this process, or -- with `group` -- one slab per rank of the group."""
     from dataclasses import replace
@@ -378,9 +392,11 @@ def run_slabs(problem, opt, solver: SolverConfig = SolverConfig(), max_levels=No
     from .errors import NumericalError
 
     if group is not None:
-        R = SlabRun.from_process_group(problem, opt, solver, max_levels, omega, init_densities, group)
+        R = SlabRun.from_process_group(problem, opt, solver, max_levels, omega, init_densities, group,
+                                       init_displacement=init_displacement)
     else:
-        R = SlabRun(problem, opt, solver, max_levels, omega, nranks=nranks, init_densities=init_densities)
+        R = SlabRun(problem, opt, solver, max_levels, omega, nranks=nranks, init_densities=init_densities,
+                    init_displacement=init_displacement)
     records: List = []
     converged = False
     iteration = start_iteration

@@ -62,3 +62,33 @@ def test_filter_kernel_matches_reference():
 
     for tag, r in (("r15", 1.5 * 0.75), ("r25", 2.5 * 0.75), ("r18", 1.8 * 0.75)):
         assert np.array_equal(O.filter_kernel(0.75, r), g[f"{tag}_kernel"])
+
+
+def test_bench_reference_arm_is_product_free():
+    """bench.py restates the config dims so its reference arm never imports the
+    product package (which would map libvoxb200.so into the reference process);
+    the restated dims must equal cases.CONFIGS, and the two arms' config dicts
+    must be the same object shape."""
+    import importlib.util
+    import subprocess
+    import sys
+
+    spec = importlib.util.spec_from_file_location("_bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_2201_12931_b200 import cases
+
+    for k, (dims, vf, lv) in bench.DIMS.items():
+        c = cases.CONFIGS[k]
+        assert (tuple(c["dims"]), c["volfrac"], c["levels"]) == (tuple(dims), vf, lv), k
+        g = c["builder"](*dims).grid
+        cfg = bench.config_of(k)
+        assert cfg["dofs"] == g.n_dofs and cfg["elements"] == g.n_elements
+    # importing bench and building the reference workload must not load the product
+    code = ("import sys, importlib.util; sys.path.insert(0, %r); "
+            "s = importlib.util.spec_from_file_location('b', %r); b = importlib.util.module_from_spec(s); "
+            "s.loader.exec_module(b); b._oracle_apply_setup('cfg1'); "
+            "assert not any(m.startswith('paper_2201_12931_b200') for m in sys.modules), 'product imported'; "
+            "maps = open('/proc/self/maps').read(); assert 'libvoxb200' not in maps, 'product .so mapped'"
+            % (ROOT, os.path.join(ROOT, "bench.py")))
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=ROOT)
