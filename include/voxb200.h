@@ -118,6 +118,17 @@ vt_status vt_residual(vt_grid *g, const double *scale, const double *u, const do
                       double *r, void *stream);
 /* out = x . y over this slab's owned dofs (deterministic order); blocking. */
 vt_status vt_dot(vt_grid *g, const double *x, const double *y, double *out, void *stream);
+/* numpy-rounded updates over a whole node vector [ref: solver.py:131-158]:
+ * mode 0 y = y + a*x, mode 1 y = y - a*x, mode 2 y = x + a*y */
+vt_status vt_axpy(vt_grid *g, int mode, double a, const double *x, double *y, void *stream);
+/* dst = src with fixed dofs zeroed (dst may equal src) [ref: solver.py:99] */
+vt_status vt_project(vt_grid *g, const double *src, double *dst, void *stream);
+/* K (n x n, device, n = n_dofs) = the dense global stiffness with identity
+ * rows / columns on fixed dofs, bit-identical to the reference's np.add.at
+ * assembly [ref: operator.py:187-205]; k0: 576 device doubles.  The caller
+ * enforces the reference's dense guard. */
+vt_status vt_assemble_dense(vt_grid *g, const double *scale, const double *k0, double *K,
+                            void *stream);
 
 /* ---------------------------------------------------------- multigrid
  * Homogenized geometric multigrid [ref: multigrid.py:150-499].  Level 0 is
@@ -254,6 +265,18 @@ vt_status vt_dist_create(vt_dist **out, int nx, int ny, int nz, double h, double
                          const uint8_t *node_mask, int levels, double omega, int nranks,
                          int rank0, int nlocal, const int *kbounds, int dist_level,
                          const uint8_t *nccl_id, int device);
+/* One slab per process with the peer-memory transport (csrc/peer.cu): every
+ * exchange is one kernel that loads the neighbours' staged planes straight
+ * from their device memory (CUDA IPC; NVLink / NVSwitch across the GPUs of a
+ * box, the same HBM when ranks share a GPU).  After creation every rank
+ * exports vt_dist_peer_handle, the handles are all-gathered (rank order) and
+ * passed to vt_dist_peer_open before the first exchange. */
+vt_status vt_dist_create_peer(vt_dist **out, int nx, int ny, int nz, double h, double nu,
+                              const uint8_t *node_mask, int levels, double omega, int nranks,
+                              int rank, const int *kbounds, int dist_level, int device);
+int vt_peer_handle_bytes(void);
+vt_status vt_dist_peer_handle(vt_dist *D, uint8_t *out, int nbytes);
+vt_status vt_dist_peer_open(vt_dist *D, const uint8_t *handles, int nbytes);
 vt_status vt_dist_destroy(vt_dist *D);
 int vt_dist_levels(const vt_dist *D);
 int vt_dist_dist_level(const vt_dist *D);

@@ -769,8 +769,11 @@ class Rec:
 
 def run_design(case: Case, volfrac, rmin, iters, tol=1e-5, maxit=200, max_levels=None,
                omega=0.4, ch_tol=0.01, move=0.2, eta=0.5, q=1.0, gamma=1e-3,
-               rho0=None, u0=None, on_iter: Optional[Callable] = None, scheme="homogenized"):
-    """SIMP loop of optimize.py:344-455 with MGPCG (homogenized or galerkin)."""
+               rho0=None, u0=None, on_iter: Optional[Callable] = None, scheme="homogenized",
+               p_continuation=False, obj_tol=None):
+    """SIMP loop of optimize.py:344-455 with MGPCG (homogenized or galerkin);
+    p_continuation ramps p = min(p, 1 + 0.5 (it // 15)) (optimize.py:78-82),
+    obj_tol adds the compliance-change stop test (optimize.py:448-453)."""
     es = case.es
     k0 = hex8_k0(case.nu, case.h)
     fixed = np.flatnonzero(case.fixed_mask)
@@ -798,11 +801,12 @@ def run_design(case: Case, volfrac, rmin, iters, tol=1e-5, maxit=200, max_levels
     recs = []
     for it in range(iters):
         t0 = time.perf_counter()
-        scale = case.E * simp(rho, case.p, case.kmin)
+        p_it = min(case.p, 1.0 + 0.5 * (it // 15)) if p_continuation else case.p
+        scale = case.E * simp(rho, p_it, case.kmin)
         f = gravity_load(rho, es, grav, f_ext, fixed) if grav is not None else f_ext
         if H is None:
             H = hier_build(es, case.h, case.fixed_mask, max_levels, omega, scheme=scheme)
-        hier_refresh(H, rho, scale, k0, case.p, case.kmin, case.E)
+        hier_refresh(H, rho, scale, k0, p_it, case.kmin, case.E)
         n = f.shape[0]
         budget = 4 * n + H.vector_scalars
         if budget > 10.5 * n:
@@ -811,7 +815,7 @@ def run_design(case: Case, volfrac, rmin, iters, tol=1e-5, maxit=200, max_levels
         rs = lambda v, ff: resid_k(v, ff, es, fixed, k0, scale)
         u, rep = pcg(ap, rs, lambda r: vcycle(H, r), f, u, fixed, tol, maxit)
         c = float(f @ u)
-        dc = sensitivities(u, rho, es, k0, case.p, case.kmin, case.E, grav)
+        dc = sensitivities(u, rho, es, k0, p_it, case.kmin, case.E, grav)
         dcf = filter_sens(dc, rho, kern, wsum, gamma, es)
         new, lam, steps = oc_update(rho, act, dcf, dv, volfrac, move, eta, q)
         ch = float(np.abs(new - rho).max())
@@ -824,7 +828,8 @@ def run_design(case: Case, volfrac, rmin, iters, tol=1e-5, maxit=200, max_levels
         recs.append(rec)
         if on_iter is not None:
             on_iter(rec, rho, u)
-        if ch <= ch_tol:
+        obj_ok = obj_tol is None or len(recs) < 2 or abs(recs[-1].compliance - recs[-2].compliance) <= obj_tol
+        if ch <= ch_tol and obj_ok:
             break
     return rho, u, recs
 

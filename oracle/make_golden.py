@@ -369,6 +369,67 @@ def gen_traj(vt, which):
             json.dump(info, fh, indent=1)
 
 
+def gen_dropin(vt):
+    """Drop-in surface beyond the hot path: assemble_dense (operator.py:187-205),
+    pcg with a user preconditioner (solver.py:62-167), p-continuation
+    (optimize.py:78-82) and the obj_tol stop (optimize.py:448-453)."""
+    from voxtop.app.presets import instantiate
+
+    rng = np.random.default_rng(77)
+    out = {}
+    for tag, dims, h in (("a", (4, 3, 2), 1.0), ("b", (6, 5, 4), 0.5)):
+        grid = vt.build_grid(*dims, h)
+        rho = rng.uniform(0.0, 1.0, grid.n_elements)
+        fixed = rng.choice(grid.n_dofs, size=grid.n_dofs // 8 + 2, replace=False)
+        st = vt.OperatorState(grid, rho, vt.MaterialModel(), fixed, vt.unit_stiffness(0.3, h))
+        out[f"dense_{tag}_dims"] = np.array(dims)
+        out[f"dense_{tag}_h"] = h
+        out[f"dense_{tag}_rho"] = rho
+        out[f"dense_{tag}_fixed"] = np.sort(fixed)
+        out[f"dense_{tag}_K"] = vt.assemble_dense(st)
+    problem, _ = instantiate("cantilever", (16, 8, 8))
+    grid = problem.grid
+    fm = problem.boundary.fixed_mask(grid)
+    f = problem.boundary.external_force(grid)
+    f[np.flatnonzero(fm)] = 0.0
+    rho = rng.uniform(0.05, 1.0, grid.n_elements)
+    st = vt.OperatorState(grid, rho, problem.model, fm, problem.stiffness())
+    d = vt.diagonal(st)
+    w = 1.0 / (2.0 * d)
+    prec = lambda r: r * w  # a user preconditioner: half-scaled Jacobi
+    x, rep = vt.pcg(st, prec, f, cfg=vt.SolverConfig(tolerance=1e-8, max_iterations=3000))
+    out["up_rho"] = rho
+    out["up_f"] = f
+    out["up_x"] = x
+    out["up_rep"] = np.array([rep.iterations, rep.final_rel_residual, rep.precond_applications,
+                              float(rep.converged)])
+    u0 = rng.standard_normal(grid.n_dofs) * 1e-2
+    x, rep = vt.pcg(st, prec, f, u0=u0, cfg=vt.SolverConfig(tolerance=1e-6, max_iterations=60))
+    out["up_u0"] = u0
+    out["upw_x"] = x
+    out["upw_rep"] = np.array([rep.iterations, rep.final_rel_residual, rep.precond_applications,
+                               float(rep.converged)])
+    h = grid.h
+    # p-continuation: p ramps 1 -> 1.5 -> 2 -> ... every 15 iterations (tight solves)
+    opt = vt.OptConfig(volfrac=0.12, filter_radius=2.5 * h, p=3.0, max_iterations=32, ch_tol=1e-12,
+                       p_continuation=True)
+    recs, snaps, wall, _ = _traj(vt, problem, opt, {32}, max_levels=3, tol=1e-10, maxit=1000)
+    out["pc_recs"] = recs
+    out["pc_rho32"] = snaps["rho32"]
+    # obj_tol: change <= 0.05 from iteration 16 on; the run stops at the first
+    # iteration that also has |c_k - c_(k-1)| <= obj_tol (iteration 25)
+    opt = vt.OptConfig(volfrac=0.12, filter_radius=2.5 * h, max_iterations=40, ch_tol=0.05, obj_tol=OBJ_TOL)
+    recs, snaps, wall, res = _traj(vt, problem, opt, set(), max_levels=3, tol=1e-10, maxit=1000)
+    out["ot_recs"] = recs
+    out["ot_rho"] = res.densities.values
+    out["ot_meta"] = np.array([res.iterations, float(res.converged), OBJ_TOL])
+    np.savez_compressed(os.path.join(OUT, "dropin.npz"), **out)
+    print("obj_tol run stopped after", res.iterations, "diffs", np.abs(np.diff(recs[:, 1]))[-4:])
+
+
+OBJ_TOL = 1000.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="k0,operator,multigrid,galerkin,io,pcg,design,small,bridge,grav,cfg1,galtraj")
@@ -377,7 +438,8 @@ def main():
     vt = _vt()
     which = set(a.only.split(","))
     for name, fn in (("k0", gen_k0), ("operator", gen_operator), ("multigrid", gen_multigrid),
-                     ("galerkin", gen_galerkin), ("io", gen_io), ("pcg", gen_pcg), ("design", gen_design)):
+                     ("galerkin", gen_galerkin), ("io", gen_io), ("pcg", gen_pcg), ("design", gen_design),
+                     ("dropin", gen_dropin)):
         if name in which:
             t = time.perf_counter()
             fn(vt)

@@ -30,7 +30,7 @@ from .mesh import (
 )
 from ._lib import lib as _native_lib  # noqa: F401  (fails loudly if the .so is missing)
 from .device import DeviceGrid, DeviceVector
-from .stiffness_op import OperatorState, apply, diagonal, residual
+from .stiffness_op import OperatorState, apply, assemble_dense, diagonal, residual
 from .hierarchy import MgHierarchy, build_hierarchy, max_feasible_levels
 from .krylov import SolveReport, SolverConfig, jacobi_preconditioner, mgcg_solve, pcg
 from .design import (

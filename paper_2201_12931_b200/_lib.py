@@ -56,6 +56,9 @@ _SIGS = {
     "vt_diagonal": (I, [P, P, P, P]),
     "vt_residual": (I, [P, P, P, P, P, P]),
     "vt_dot": (I, [P, P, P, C.POINTER(D), P]),
+    "vt_axpy": (I, [P, I, D, P, P, P]),
+    "vt_project": (I, [P, P, P, P]),
+    "vt_assemble_dense": (I, [P, P, P, P, P]),
     "vt_hier_create": (I, [C.POINTER(P), P, I, D, I]),
     "vt_hier_destroy": (I, [P]),
     "vt_hier_create_ex": (I, [C.POINTER(P), P, I, D, I, I]),
@@ -90,6 +93,10 @@ _SIGS = {
     "vt_nccl_id_bytes": (I, []),
     "vt_nccl_unique_id": (I, [P, I]),
     "vt_dist_create": (I, [C.POINTER(P), I, I, I, D, D, P, I, D, I, I, I, P, I, P, I]),
+    "vt_dist_create_peer": (I, [C.POINTER(P), I, I, I, D, D, P, I, D, I, I, P, I, I]),
+    "vt_peer_handle_bytes": (I, []),
+    "vt_dist_peer_handle": (I, [P, P, I]),
+    "vt_dist_peer_open": (I, [P, P, I]),
     "vt_dist_destroy": (I, [P]),
     "vt_dist_levels": (I, [P]),
     "vt_dist_dist_level": (I, [P]),

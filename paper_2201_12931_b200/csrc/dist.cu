@@ -117,6 +117,9 @@ vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStrea
   const Geom& g = S.lv[l]->g;
   const int r = S.rank, n = g.k1 - g.k0;
   double* x = v[0];
+  if (D->px)
+    return peer_halo(D, x + (size_t)g.nplane, x + (size_t)n * g.nplane, x, x + (size_t)(n + 1) * g.nplane,
+                     g.nplane, s);
   auto& A = nccl();
   VT_NCCL(A.GroupStart());
   if (r > 0) {
@@ -145,6 +148,18 @@ vt_status halo_elems(vt_dist* D, int l, const std::vector<double*>& e, cudaStrea
   const DSlab& S = D->sl[0];
   const Geom& g = S.lv[l]->g;
   const int r = S.rank, n = g.k1 - g.k0;
+  if (D->px) {  // only the layer below travels (rank+1 pulls my top layer)
+    PeerOps o;
+    if (r < D->N - 1) {
+      o.pack(e[0] + (size_t)n * g.eplane, (long long)D->px->half, g.eplane);
+      o.wait(r + 1);
+    }
+    if (r > 0) {
+      o.pull(r - 1, (long long)D->px->half, e[0], g.eplane);
+      o.wait(r - 1);
+    }
+    return peer_exchange(D, o, s);
+  }
   auto& A = nccl();
   VT_NCCL(A.GroupStart());
   if (r < D->N - 1) VT_NCCL(A.Send(e[0] + (size_t)n * g.eplane, g.eplane, ncclDouble, r + 1, D->comm, s));
@@ -157,6 +172,12 @@ vt_status halo_elems(vt_dist* D, int l, const std::vector<double*>& e, cudaStrea
 vt_status gather_scal(vt_dist* D, int slot, cudaStream_t s) {
   if (!D->remote()) return VT_OK;
   double* base = D->scal + (size_t)slot * D->N;
+  if (D->px) {
+    PeerOps o = peer_all_but_self(D);
+    o.pack(base + D->sl[0].rank, 0, 1);
+    for (int i = 0; i < o.nwait; ++i) o.pull(o.wpeer[i], 0, base + o.wpeer[i], 1);
+    return peer_exchange(D, o, s);
+  }
   VT_NCCL(nccl().AllGather(base + D->sl[0].rank, base, 1, ncclDouble, D->comm, s));
   return VT_OK;
 }
@@ -176,6 +197,7 @@ vt_status host_slot_sum(vt_dist* D, int slot, cudaStream_t s, double* out) {
   VT_CUDA(cudaMemcpyAsync(D->host_scal, D->scal + (size_t)slot * D->N, D->N * sizeof(double),
                           cudaMemcpyDeviceToHost, s));
   VT_CUDA(cudaStreamSynchronize(s));
+  VT_TRY(peer_check(D));
   double acc = 0.0;
   for (int g = 0; g < D->N; ++g) acc += D->host_scal[g];
   *out = acc;
@@ -187,7 +209,7 @@ vt_status host_slot_values(vt_dist* D, int slot, cudaStream_t s, double* out) {
   VT_CUDA(cudaMemcpyAsync(out, D->scal + (size_t)slot * D->N, D->N * sizeof(double),
                           cudaMemcpyDeviceToHost, s));
   VT_CUDA(cudaStreamSynchronize(s));
-  return VT_OK;
+  return peer_check(D);
 }
 
 // tail-level rhs ranges written by each rank -> every rank
@@ -195,6 +217,23 @@ static vt_status gather_tail_f(vt_dist* D, cudaStream_t s) {
   if (!D->remote()) return VT_OK;
   vt_grid* C = D->tail->lv[1];
   double* f = D->tail->f[1];
+  auto range = [&](int r, int* kb, int* ke) {
+    const int a = lvl_k(D->kb[r], D->D), b = lvl_k(D->kb[r + 1], D->D) + (r == D->N - 1 ? 1 : 0);
+    *kb = (a + 1) / 2;
+    *ke = (b + 1) / 2;
+  };
+  if (D->px) {
+    PeerOps o = peer_all_but_self(D);
+    int kb, ke;
+    range(D->sl[0].rank, &kb, &ke);
+    if (ke > kb) o.pack(f + (size_t)(kb + 1) * C->g.nplane, 0, (long long)(ke - kb) * C->g.nplane);
+    for (int i = 0; i < o.nwait; ++i) {
+      range(o.wpeer[i], &kb, &ke);
+      if (ke > kb)
+        o.pull(o.wpeer[i], 0, f + (size_t)(kb + 1) * C->g.nplane, (long long)(ke - kb) * C->g.nplane);
+    }
+    return peer_exchange(D, o, s);
+  }
   auto& A = nccl();
   VT_NCCL(A.GroupStart());
   for (int r = 0; r < D->N; ++r) {
@@ -387,17 +426,20 @@ vt_status vt_nccl_unique_id(uint8_t* out, int nbytes) {
 
 int vt_nccl_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
 
-vt_status vt_dist_create(vt_dist** out, int nx, int ny, int nz, double h, double nu,
-                         const uint8_t* node_mask, int levels, double omega, int nranks,
-                         int rank0, int nlocal, const int* kbounds, int dist_level,
-                         const uint8_t* nccl_id, int device) {
+}  // extern "C"
+
+static vt_status dist_create(vt_dist** out, int nx, int ny, int nz, double h, double nu,
+                             const uint8_t* node_mask, int levels, double omega, int nranks,
+                             int rank0, int nlocal, const int* kbounds, int dist_level,
+                             const uint8_t* nccl_id, bool peer, int device) {
   if (!out || !node_mask || !kbounds) return fail(VT_EINVAL, "null argument");
   if (nranks < 1 || nlocal < 1 || rank0 < 0 || rank0 + nlocal > nranks)
     return fail(VT_EINVAL, "bad rank layout");
-  if (nccl_id == nullptr && nlocal != nranks)
-    return fail(VT_EINVAL, "without a communicator every slab must live in this process");
-  if (nccl_id != nullptr && nlocal != 1)
-    return fail(VT_EINVAL, "with a communicator each process owns exactly one slab");
+  const bool multi = nccl_id != nullptr || peer;
+  if (!multi && nlocal != nranks)
+    return fail(VT_EINVAL, "without a transport every slab must live in this process");
+  if (multi && nlocal != 1)
+    return fail(VT_EINVAL, "with a multi-process transport each process owns exactly one slab");
   if (levels < 2) return fail(VT_EINVAL, "the slab solver needs at least 2 multigrid levels");
   if (dist_level < 0 || dist_level > levels - 2)
     return fail(VT_EINVAL, "distributed levels must leave a replicated coarse tail");
@@ -493,9 +535,48 @@ vt_status vt_dist_create(vt_dist** out, int nx, int ny, int nz, double h, double
     return bail(fail(VT_ENOMEM, "control block alloc"));
   if (cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(VT_ECUDA, "stream create"));
+  if (peer) {
+    // staging: halves large enough for a level-0 node plane, an element layer
+    // and PEER_MAX_R filter layers; the whole area for one rank's share of the
+    // tail right-hand side / the level-D densities
+    const Geom& g0 = D->sl[0].lv[0]->g;
+    const long long layer = (long long)nx * ny;
+    long long half = g0.nplane;
+    half = half > g0.eplane ? half : g0.eplane;
+    half = half > PEER_MAX_R * layer ? half : PEER_MAX_R * layer;
+    long long whole = 2 * half;
+    vt_grid* C = D->tail->lv[1];
+    const long long per_layer = (long long)(nx >> dist_level) * (ny >> dist_level);
+    for (int r = 0; r < nranks; ++r) {
+      const int a = kbounds[r] >> dist_level, b = (kbounds[r + 1] >> dist_level) + (r == nranks - 1 ? 1 : 0);
+      const long long tf = (long long)((b + 1) / 2 - (a + 1) / 2) * C->g.nplane;
+      const long long rd = (long long)((kbounds[r + 1] - kbounds[r]) >> dist_level) * per_layer;
+      whole = whole > tf ? whole : tf;
+      whole = whole > rd ? whole : rd;
+    }
+    st = peer_init(D, (size_t)(whole + (whole & 1)));
+    if (st != VT_OK) return bail(st);
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(VT_ECUDA, "dist setup"));
   *out = D;
   return VT_OK;
+}
+
+extern "C" {
+
+vt_status vt_dist_create(vt_dist** out, int nx, int ny, int nz, double h, double nu,
+                         const uint8_t* node_mask, int levels, double omega, int nranks,
+                         int rank0, int nlocal, const int* kbounds, int dist_level,
+                         const uint8_t* nccl_id, int device) {
+  return dist_create(out, nx, ny, nz, h, nu, node_mask, levels, omega, nranks, rank0, nlocal, kbounds,
+                     dist_level, nccl_id, false, device);
+}
+
+vt_status vt_dist_create_peer(vt_dist** out, int nx, int ny, int nz, double h, double nu,
+                              const uint8_t* node_mask, int levels, double omega, int nranks,
+                              int rank, const int* kbounds, int dist_level, int device) {
+  return dist_create(out, nx, ny, nz, h, nu, node_mask, levels, omega, nranks, rank, 1, kbounds,
+                     dist_level, nullptr, true, device);
 }
 
 vt_status vt_dist_destroy(vt_dist* D) {
@@ -523,6 +604,7 @@ vt_status vt_dist_destroy(vt_dist* D) {
   for (double* p : D->fprod) cudaFree(p);
   for (double* p : D->gpad) cudaFree(p);
   if (D->comm) nccl().CommDestroy(D->comm);
+  peer_free(D);
   delete D;
   return VT_OK;
 }
@@ -587,6 +669,20 @@ vt_status vt_dist_refresh(vt_dist* D, const double* const* rho, const double* co
       VT_CUDA(cudaMemcpyAsync(D->rho_full + (long long)G->g.k0 * per_layer, S.rho[D->D],
                               G->nel_local() * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
+  } else if (D->px) {
+    PeerOps o = peer_all_but_self(D);
+    const DSlab& S = D->sl[0];
+    const long long own = (long long)(D->kb[S.rank] >> D->D) * per_layer;
+    VT_CUDA(cudaMemcpyAsync(D->rho_full + own, S.rho[D->D], S.lv[D->D]->nel_local() * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+    o.pack(S.rho[D->D], 0, S.lv[D->D]->nel_local());
+    for (int i = 0; i < o.nwait; ++i) {
+      const int r = o.wpeer[i];
+      const long long a = (long long)(D->kb[r] >> D->D) * per_layer;
+      const long long b = (long long)(D->kb[r + 1] >> D->D) * per_layer;
+      o.pull(r, 0, D->rho_full + a, b - a);
+    }
+    VT_TRY(peer_exchange(D, o, s));
   } else {
     auto& A = nccl();
     VT_CUDA(cudaMemcpyAsync(D->rho_full + (long long)(D->kb[D->sl[0].rank] >> D->D) * per_layer,
@@ -604,6 +700,7 @@ vt_status vt_dist_refresh(vt_dist* D, const double* const* rho, const double* co
   int hb = 0;
   VT_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   VT_CUDA(cudaStreamSynchronize(s));
+  VT_TRY(peer_check(D));
   if (hb) return fail(VT_EDENSITY, "density outside [0, 1]");
   VT_TRY(vt_hier_refresh(D->tail, D->rho_full, D->scale_full, p, kmin, E, stream));
   D->refreshed = true;
@@ -690,7 +787,7 @@ vt_status vt_dist_pcg(vt_dist* D, const double* const* f, double* const* x, int 
       VT_CUDA(cudaMemcpyAsync(x[i], D->sl[i].x, D->sl[i].lv[0]->vec_len() * sizeof(double),
                               cudaMemcpyDeviceToDevice, s));
     VT_CUDA(cudaStreamSynchronize(s));
-    return VT_OK;
+    return peer_check(D);
   };
   if (fnorm == 0.0) {
     VT_TRY(finish());
@@ -774,6 +871,7 @@ vt_status vt_dist_pcg(vt_dist* D, const double* const* f, double* const* x, int 
     }
     cudaError_t e = cudaEventSynchronize(ev[i & 1]);
     if (e != cudaSuccess) { st = cuda_fail(e, "dist pcg iteration"); break; }
+    if ((st = peer_check(D)) != VT_OK) break;
     if (ring[i & 1].stop) break;
   }
   cudaStreamSynchronize(s);

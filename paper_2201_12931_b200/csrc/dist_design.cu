@@ -181,6 +181,8 @@ static vt_status halo_prod(vt_dist* D, cudaStream_t s) {
   }
   const int r = D->sl[0].rank, n = nl(0);
   double* p = D->fprod[0];
+  if (D->px)
+    return peer_halo(D, p + blk, p + (size_t)n * layer, p, p + (size_t)(R + n) * layer, (long long)blk, s);
   auto& A = nccl();
   VT_NCCL(A.GroupStart());
   if (r > 0) {
@@ -273,6 +275,18 @@ vt_status vt_dist_gravity_load(vt_dist* D, const double* const* rho, int grav_ax
       for (int i = 1; i < D->N; ++i)
         VT_CUDA(cudaMemcpyAsync(D->gpad[i], D->gpad[i - 1] + (size_t)nl(i - 1) * layer,
                                 layer * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else if (D->px) {  // rank+1 pulls my top layer, I pull rank-1's
+      const int r = D->sl[0].rank;
+      PeerOps o;
+      if (r < D->N - 1) {
+        o.pack(D->gpad[0] + (size_t)nl(0) * layer, (long long)D->px->half, layer);
+        o.wait(r + 1);
+      }
+      if (r > 0) {
+        o.pull(r - 1, (long long)D->px->half, D->gpad[0], layer);
+        o.wait(r - 1);
+      }
+      VT_TRY(peer_exchange(D, o, s));
     } else {
       const int r = D->sl[0].rank;
       auto& A = nccl();
@@ -296,6 +310,8 @@ vt_status vt_dist_gravity_load(vt_dist* D, const double* const* rho, int grav_ax
 // sensitivity filter of half-width R (kernel in (dk, dj, di) order) [ref: optimize.py:110-171]
 vt_status vt_dist_filter_create(vt_dist* D, int R, const double* kernel_host) {
   if (R < 0) return fail(VT_EINVAL, "filter half-width must be non-negative");
+  if (D->px && R > PEER_MAX_R)
+    return fail(VT_EINVAL, "filter half-width exceeds the peer transport's staging area (8 layers)");
   for (int i = 0; i < D->nlocal; ++i) {
     const Geom& g = D->sl[i].lv[0]->g;
     if (D->N > 1 && g.k1 - g.k0 < R)

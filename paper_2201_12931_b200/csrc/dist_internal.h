@@ -42,6 +42,55 @@ struct DSlab {
 
 constexpr int NSLOT = 16;
 
+// ------------------------------------------------------------------ peer transport (peer.cu)
+constexpr int XP_MAXOPS = 16;
+constexpr int PEER_MAX_R = 8;  // filter half-widths the peer staging area holds
+
+// one exchange: pack own data into the staging area, pull peers' staged data
+struct PeerOps {
+  int npack = 0, npull = 0, nwait = 0;
+  const double* psrc[XP_MAXOPS];
+  long long poff[XP_MAXOPS], pn[XP_MAXOPS];  // staging offset / count (doubles)
+  int qpeer[XP_MAXOPS];
+  long long qoff[XP_MAXOPS], qn[XP_MAXOPS];
+  double* qdst[XP_MAXOPS];
+  int wpeer[XP_MAXOPS];                       // ranks synchronised with (symmetric)
+  void pack(const double* src, long long off, long long n) {
+    psrc[npack] = src; poff[npack] = off; pn[npack] = n; ++npack;
+  }
+  void pull(int peer, long long off, double* dst, long long n) {
+    qpeer[npull] = peer; qoff[npull] = off; qdst[npull] = dst; qn[npull] = n; ++npull;
+  }
+  void wait(int peer) { wpeer[nwait++] = peer; }
+};
+
+struct XArgs {
+  int npack, npull, nwait;
+  const double* psrc[XP_MAXOPS];
+  long long poff[XP_MAXOPS], pn[XP_MAXOPS];
+  const double* qsrc[XP_MAXOPS];
+  double* qdst[XP_MAXOPS];
+  long long qn[XP_MAXOPS];
+  unsigned long long* wflag[XP_MAXOPS];
+  double* stage;
+  unsigned long long* self;   // own flags: [0] ready, [1] done
+  unsigned long long* ctr;    // local: [0] epoch
+  unsigned* cnt;              // local: [0] packers, [1] pullers
+  int* err;                   // mapped host word
+  unsigned long long timeout_ns;
+};
+
+struct PeerXport {
+  void* block = nullptr;              // IPC-shared: 256 B flags + staging
+  void* local = nullptr;              // epoch + CTA counters (not shared)
+  size_t stage_doubles = 0, half = 0; // staging area; halo exchanges use [0, half) down, [half, 2 half) up
+  std::vector<void*> peer_block;      // every rank's block in this address space
+  int* err_host = nullptr;
+  int* err_dev = nullptr;
+  unsigned long long timeout_ns = 0;
+  bool opened = false;
+};
+
 }  // namespace vt
 
 struct vt_dist {
@@ -70,7 +119,9 @@ struct vt_dist {
   double* opart = nullptr;              // OC / change partials (per slab, 4096 x 4)
   std::vector<double*> gpad;            // per slab: rho with the element layer below (gravity)
 
-  bool remote() const { return comm != nullptr; }
+  vt::PeerXport* px = nullptr;         // peer-memory transport (peer.cu), else NCCL when comm
+
+  bool remote() const { return comm != nullptr || px != nullptr; }
 };
 
 namespace vt {
@@ -90,4 +141,13 @@ vt_status slab_sum(vt_dist* D, int i, const double* partial, int n, int n50, int
                    const PcgCtl* ctl, cudaStream_t s);
 vt_status host_slot_sum(vt_dist* D, int slot, cudaStream_t s, double* out);
 vt_status host_slot_values(vt_dist* D, int slot, cudaStream_t s, double* out);
+vt_status peer_init(vt_dist* D, size_t stage_doubles);
+void peer_free(vt_dist* D);
+vt_status peer_check(vt_dist* D);
+vt_status peer_exchange(vt_dist* D, const PeerOps& ops, cudaStream_t s);
+PeerOps peer_all_but_self(vt_dist* D);
+// neighbour halo: send `down` (n doubles) to rank-1 and `up` to rank+1, receive
+// rank-1's `up` into below and rank+1's `down` into above
+vt_status peer_halo(vt_dist* D, const double* down, const double* up, double* below, double* above,
+                    long long n, cudaStream_t s);
 }  // namespace vt

@@ -422,6 +422,21 @@ vt_status vt_dot(vt_grid* G, const double* x, const double* y, double* out, void
   return VT_OK;
 }
 
+vt_status vt_axpy(vt_grid* G, int mode, double a, const double* x, double* y, void* stream) {
+  if (mode < 0 || mode > 2) return fail(VT_EINVAL, "axpy mode must be 0, 1 or 2");
+  return launch_axpy(G, mode, a, x, y, (cudaStream_t)stream);
+}
+
+vt_status vt_project(vt_grid* G, const double* src, double* dst, void* stream) {
+  return launch_project(G, src, dst, (cudaStream_t)stream);
+}
+
+vt_status vt_assemble_dense(vt_grid* G, const double* scale, const double* k0, double* K,
+                            void* stream) {
+  if (G->g.k0 != 0 || G->g.k1 != G->g.nz) return fail(VT_EINVAL, "dense assembly needs the whole grid");
+  return launch_assemble_dense(G, scale, k0, K, (cudaStream_t)stream);
+}
+
 vt_status vt_compliance(vt_grid* G, const double* f, const double* u, double* c, void* stream) {
   return vt_dot(G, f, u, c, stream);
 }

@@ -113,6 +113,73 @@ vt_status launch_zero_owned(vt_grid* G, double* v, cudaStream_t s) {
   return VT_OK;
 }
 
+// ---------------------------------------------------------------- axpy
+// numpy-rounded vector updates over the whole vt vector (ghosts / pads stay 0):
+//   mode 0: y = y + a*x   (`y += a * x`)     mode 1: y = y - a*x   (`y -= a * x`)
+//   mode 2: y = x + a*y   (`y = x + a * y`)
+__global__ void axpy_kernel(long long n, int mode, double a, const double* __restrict__ x,
+                            double* __restrict__ y) {
+  griddep_wait();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double yi = y[i], xi = x[i];
+    if (mode == 0) y[i] = __dadd_rn(yi, __dmul_rn(a, xi));
+    else if (mode == 1) y[i] = __dsub_rn(yi, __dmul_rn(a, xi));
+    else y[i] = __dadd_rn(xi, __dmul_rn(a, yi));
+  }
+}
+vt_status launch_axpy(vt_grid* G, int mode, double a, const double* x, double* y, cudaStream_t s) {
+  const long long n = (long long)G->vec_len();
+  launch_pdl(axpy_kernel, fit_grid(n, VT_THREADS, G->nsm * 8), VT_THREADS, 0, s, n, mode, a, x, y);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+// Dense global stiffness with identity rows / columns on fixed dofs
+// [ref: operator.py:187-205].  One CTA of 576 threads walks the elements in the
+// reference's order; thread (a, b) adds s_e K0[a][b] into K[dof_a][dof_b].
+// An element's 24 dofs are distinct, so its 576 targets are too, and the
+// barrier per element makes every entry accumulate in ascending element order
+// -- the order of np.add.at -- so K is bit-identical to the reference's.
+__global__ void __launch_bounds__(576, 1)
+    assemble_dense_kernel(Geom g, const double* scale, const double* k0, const uint8_t* mask, int n,
+                          double* K) {
+  griddep_wait();
+  const int nx1 = g.nx + 1, ny1 = g.ny + 1;
+  const long long nn = (long long)n * n;
+  for (long long t = threadIdx.x; t < nn; t += blockDim.x) K[t] = 0.0;
+  __syncthreads();
+  const int t = threadIdx.x, a = t / 24, b = t % 24, ca = a / 3, cb = b / 3;
+  const double kab = k0[t];
+  const int nel = g.nx * g.ny * (g.k1 - g.k0);
+  for (int e = 0; e < nel; ++e) {
+    const int i = e % g.nx, j = (e / g.nx) % g.ny, k = e / (g.nx * g.ny);
+    const double s = scale[elem_off(g, k + 1, j, i)];
+    const long long na = (i + (ca & 1)) + (long long)(j + ((ca >> 1) & 1)) * nx1 + (long long)(k + (ca >> 2)) * nx1 * ny1;
+    const long long nb = (i + (cb & 1)) + (long long)(j + ((cb >> 1) & 1)) * nx1 + (long long)(k + (cb >> 2)) * nx1 * ny1;
+    double* dst = K + (3 * na + a % 3) * n + 3 * nb + b % 3;
+    *dst = __dadd_rn(*dst, __dmul_rn(s, kab));
+    __syncthreads();
+  }
+  // fixed rows / columns -> identity
+  for (long long q = threadIdx.x; q < nn; q += blockDim.x) {
+    const int r = (int)(q / n), c = (int)(q % n);
+    const int nr = r / 3, nc = c / 3;
+    const unsigned mr = mask[mask_off(g, nr / (nx1 * ny1) + 1, (nr / nx1) % ny1, nr % nx1)];
+    const unsigned mc = mask[mask_off(g, nc / (nx1 * ny1) + 1, (nc / nx1) % ny1, nc % nx1)];
+    if (((mr >> (r % 3)) & 1u) || ((mc >> (c % 3)) & 1u)) K[q] = (r == c) ? 1.0 : 0.0;
+  }
+}
+vt_status launch_assemble_dense(vt_grid* G, const double* scale, const double* k0, double* K,
+                                cudaStream_t s) {
+  const int n = (int)(3LL * (G->g.nx + 1) * (G->g.ny + 1) * (G->g.k1 - G->g.k0 + 1));
+  launch_pdl(assemble_dense_kernel, 1, 576, 0, s, G->g, scale, k0, G->mask, n, K);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 // ---------------------------------------------------------------- dots
 __global__ void dot_kernel(Geom g, const double* __restrict__ x, const double* __restrict__ y,
                            double* partial, const int* stop) {

@@ -160,6 +160,9 @@ vt_status launch_hex8(vt_grid* G, int mode, bool dot, const double* scale, const
                       int pend = -1);
 // (vectors.cu)
 vt_status launch_project(vt_grid* G, const double* src, double* dst, cudaStream_t s);
+vt_status launch_axpy(vt_grid* G, int mode, double a, const double* x, double* y, cudaStream_t s);
+vt_status launch_assemble_dense(vt_grid* G, const double* scale, const double* k0, double* K,
+                                cudaStream_t s);
 vt_status launch_unpack_project(vt_grid* G, const double* dense, int pa, int pb, double* raw,
                                 double* proj, cudaStream_t s);
 vt_status launch_pack(vt_grid* G, const double* src, int pa, int pb, double* dense, cudaStream_t s);

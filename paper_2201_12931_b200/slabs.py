@@ -8,14 +8,19 @@ dense coarsest solve, is replicated on every rank; dot products are reduced
 per rank, all-gathered and summed in rank order so every rank takes the same
 scalar decisions.
 
-Two transports, same arithmetic:
+Three transports, same arithmetic:
   * ``SlabSolver(..., nranks=N)`` without a process group keeps all N slabs in
     this process on one GPU (halos are device copies) -- used by the parity
     tests, which compare it with the single-slab solve;
-  * ``SlabSolver.from_process_group(...)`` runs one slab per rank of an
-    initialised ``torch.distributed`` group (torchrun, one process per GPU);
-    the library creates its own NCCL communicator from an id broadcast over
-    that group.
+  * ``SlabSolver.from_process_group(..., transport="peer")`` (the default)
+    runs one slab per rank of an initialised ``torch.distributed`` group
+    (torchrun, one process per GPU); each exchange is one kernel that loads
+    the neighbours' staged planes from their device memory (CUDA IPC over
+    NVLink / NVSwitch; csrc/peer.cu).  The IPC handles travel over the group.
+    Ranks may also share one GPU, which is how the multi-process path is
+    tested on a single B200;
+  * ``transport="nccl"``: the same with NCCL send/recv/broadcast/all-gather
+    on a library-owned communicator (id broadcast over the group).
 
 ``plan_slabs`` (pure host logic, gloo-tested on CPU) chooses the partition.
 """
@@ -110,7 +115,7 @@ class SlabSolver:
 
     def __init__(self, grid: StructuredGrid, fixed_mask, levels: Optional[int] = None, omega: float = 0.4,
                  nranks: int = 1, rank: int = 0, nlocal: Optional[int] = None, nccl_id: Optional[bytes] = None,
-                 nu: float = 0.3, device: Optional[int] = None):
+                 nu: float = 0.3, device: Optional[int] = None, peer: bool = False):
         require_cuda()
         self.grid = grid
         self.levels = int(levels) if levels is not None else max_feasible_levels(grid.nelx, grid.nely, grid.nelz)
@@ -128,9 +133,18 @@ class SlabSolver:
         if nccl_id is not None:
             idbuf = (C.c_uint8 * len(nccl_id)).from_buffer_copy(nccl_id)
         self._h = C.c_void_p()
-        check(lib.vt_dist_create(C.byref(self._h), grid.nelx, grid.nely, grid.nelz, grid.h, nu,
-                                 nm.ctypes.data_as(C.c_void_p), self.levels, omega, nranks, rank,
-                                 self.nlocal, kb, self.plan.dist_level, idbuf, self.device), "vt_dist_create")
+        self.transport = "peer" if peer else ("nccl" if nccl_id is not None else "local")
+        if peer:
+            if self.nlocal != 1:
+                raise ValueError("the peer transport runs one slab per process")
+            check(lib.vt_dist_create_peer(C.byref(self._h), grid.nelx, grid.nely, grid.nelz, grid.h, nu,
+                                          nm.ctypes.data_as(C.c_void_p), self.levels, omega, nranks, rank, kb,
+                                          self.plan.dist_level, self.device), "vt_dist_create_peer")
+        else:
+            check(lib.vt_dist_create(C.byref(self._h), grid.nelx, grid.nely, grid.nelz, grid.h, nu,
+                                     nm.ctypes.data_as(C.c_void_p), self.levels, omega, nranks, rank,
+                                     self.nlocal, kb, self.plan.dist_level, idbuf, self.device),
+                  "vt_dist_create")
         self.slab_grids = []
         for i in range(self.nlocal):
             g = lib.vt_dist_grid(self._h, i, 0)
@@ -144,12 +158,21 @@ class SlabSolver:
         self.model: Optional[MaterialModel] = None
 
     @classmethod
-    def from_process_group(cls, grid: StructuredGrid, fixed_mask, levels=None, omega=0.4, group=None):
-        """One slab per rank of the initialised torch.distributed group; the
-        library's NCCL communicator is bootstrapped from an id broadcast over it."""
+    def from_process_group(cls, grid: StructuredGrid, fixed_mask, levels=None, omega=0.4, group=None,
+                           transport: str = "peer", nu: float = 0.3):
+        """One slab per rank of the initialised torch.distributed group.
+        transport="peer": IPC handles of every rank's staging block are
+        all-gathered over the group; "nccl": the library's NCCL communicator is
+        bootstrapped from an id broadcast over it."""
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if transport == "peer":
+            S = cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nu=nu, peer=True)
+            S.connect_peers(group)
+            return S
+        if transport != "nccl":
+            raise ValueError(f"unknown transport {transport!r}")
         nbytes = int(lib.vt_nccl_id_bytes())
         obj = [None]
         if rank == 0:
@@ -157,7 +180,21 @@ class SlabSolver:
             check(lib.vt_nccl_unique_id(buf, nbytes), "vt_nccl_unique_id")
             obj[0] = bytes(buf)
         dist.broadcast_object_list(obj, src=0, group=group)
-        return cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nccl_id=obj[0])
+        return cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nccl_id=obj[0], nu=nu)
+
+    def connect_peers(self, group=None):
+        """All-gather the ranks' IPC handles over `group` and map the peers'
+        staging blocks (peer transport)."""
+        import torch.distributed as dist
+
+        hb = int(lib.vt_peer_handle_bytes())
+        buf = (C.c_uint8 * hb)()
+        check(lib.vt_dist_peer_handle(self._h, buf, hb), "vt_dist_peer_handle")
+        allh = [None] * self.nranks
+        dist.all_gather_object(allh, bytes(buf), group=group)
+        cat = b"".join(allh)
+        arr = (C.c_uint8 * len(cat)).from_buffer_copy(cat)
+        check(lib.vt_dist_peer_open(self._h, arr, len(cat)), "vt_dist_peer_open")
 
     def close(self):
         if getattr(self, "_h", None):
@@ -258,7 +295,7 @@ class SlabRun:
 
     def __init__(self, problem, opt, solver: SolverConfig, max_levels=None, omega: float = 0.4,
                  nranks: int = 1, rank: int = 0, nlocal: Optional[int] = None, nccl_id: Optional[bytes] = None,
-                 init_densities=None, group=None, init_displacement=None):
+                 init_densities=None, group=None, init_displacement=None, peer: bool = False):
         from .design import filter_weights, initial_densities
 
         if solver.preconditioner != "multigrid":
@@ -267,7 +304,9 @@ class SlabRun:
         self.problem, self.opt, self.solver, self.group = problem, opt, solver, group
         fm = problem.boundary.fixed_mask(grid)
         self.S = S = SlabSolver(grid, fm, max_levels, omega, nranks=nranks, rank=rank, nlocal=nlocal,
-                                nccl_id=nccl_id, nu=problem.nu)
+                                nccl_id=nccl_id, nu=problem.nu, peer=peer)
+        if peer:
+            S.connect_peers(group)
         f_ext = problem.boundary.external_force(grid)
         f_ext[fm] = 0.0
         self.f_ext = S.upload(f_ext)
@@ -300,10 +339,15 @@ class SlabRun:
 
     @classmethod
     def from_process_group(cls, problem, opt, solver, max_levels=None, omega=0.4, init_densities=None,
-                           group=None, init_displacement=None):
+                           group=None, init_displacement=None, transport: str = "peer"):
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if transport == "peer":
+            return cls(problem, opt, solver, max_levels, omega, nranks=world, rank=rank, nlocal=1,
+                       init_densities=init_densities, group=group, init_displacement=init_displacement, peer=True)
+        if transport != "nccl":
+            raise ValueError(f"unknown transport {transport!r}")
         obj = [None]
         if rank == 0:
             n = int(lib.vt_nccl_id_bytes())
@@ -360,8 +404,11 @@ class SlabRun:
             return torch.cat(parts)
         import torch.distributed as dist
 
-        out = [torch.empty_like(parts[0]) for _ in range(self.S.nranks)]
-        dist.all_gather(out, parts[0].contiguous(), group=self.group)
+        x = parts[0].contiguous()
+        if dist.get_backend(self.group) != "nccl":  # gloo gathers host tensors
+            x = x.cpu()
+        out = [torch.empty_like(x) for _ in range(self.S.nranks)]
+        dist.all_gather(out, x, group=self.group)
         return torch.cat(out)
 
     def densities(self) -> np.ndarray:
@@ -383,9 +430,10 @@ class SlabRun:
 
 def run_slabs(problem, opt, solver: SolverConfig = SolverConfig(), max_levels=None, omega: float = 0.4,
               nranks: int = 1, group=None, init_densities=None, start_iteration: int = 0, on_iteration=None,
-              init_displacement=None):
+              init_displacement=None, transport: str = "peer"):
     """run() (optimize.py:323-455, homogenized scheme) on z-slabs: all `nranks`
-    slabs in this process, or -- with `group` -- one slab per rank of the group."""
+    slabs in this process, or -- with `group` -- one slab per rank of the group
+    over the `transport` ("peer" or "nccl")."""
     from dataclasses import replace
 
     from .design import DensityField, OptResult, RunRecord, VOLUME_TOL
@@ -393,7 +441,7 @@ def run_slabs(problem, opt, solver: SolverConfig = SolverConfig(), max_levels=No
 
     if group is not None:
         R = SlabRun.from_process_group(problem, opt, solver, max_levels, omega, init_densities, group,
-                                       init_displacement=init_displacement)
+                                       init_displacement=init_displacement, transport=transport)
     else:
         R = SlabRun(problem, opt, solver, max_levels, omega, nranks=nranks, init_densities=init_densities,
                     init_displacement=init_displacement)

@@ -21,7 +21,10 @@ from .device import DeviceGrid, DeviceVector, device_grid, ptr, require_cuda, st
 from .material import ElementStiffness, MaterialModel, unit_stiffness
 from .mesh import StructuredGrid
 
-__all__ = ["OperatorState", "apply", "diagonal", "residual", "as_device", "from_device"]
+__all__ = ["OperatorState", "apply", "diagonal", "residual", "assemble_dense", "as_device", "from_device",
+           "DENSE_GUARD_DOFS"]
+
+DENSE_GUARD_DOFS = 20_000  # [ref: operator.py:28]
 
 
 def _check_stiffness(st: ElementStiffness, grid: StructuredGrid):
@@ -159,3 +162,20 @@ def residual(state: OperatorState, u, f):
     r = d.zeros()
     check(lib.vt_residual(d.handle, ptr(state.scale_dev), ptr(ud), ptr(fd), ptr(r), stream_ptr()))
     return from_device(d, r, u)
+
+
+def assemble_dense(state: OperatorState, guard: int = DENSE_GUARD_DOFS) -> np.ndarray:
+    """Explicit global stiffness with identity rows/columns on fixed dofs
+    (operator.py:187-205).  Assembled on the device in the reference's
+    element order, so the result is bit-identical to its np.add.at sum;
+    refuses grids above the guard limit like the reference."""
+    n = state.grid.n_dofs
+    if n > guard:
+        raise ValueError(f"dense assembly of {n} dofs exceeds the guard limit {guard}")
+    d = state.dgrid
+    k0 = torch.as_tensor(np.ascontiguousarray(state.stiffness.matrix, dtype=np.float64).reshape(-1),
+                         device=f"cuda:{d.device}")
+    K = torch.empty((n, n), dtype=torch.float64, device=f"cuda:{d.device}")
+    check(lib.vt_assemble_dense(d.handle, ptr(state.scale_dev), ptr(k0), ptr(K), stream_ptr()),
+          "vt_assemble_dense")
+    return K.cpu().numpy()

@@ -1,0 +1,97 @@
+"""The drop-in surface beyond the hot path, on the GPU, against reference
+fixtures (tests/golden/dropin.npz, made by oracle/make_golden.py --only dropin):
+assemble_dense (operator.py:187-205), pcg with a user preconditioner
+(solver.py:62-167), p-continuation (optimize.py:78-82) and the obj_tol stop
+(optimize.py:448-453)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+vb = pytest.importorskip("paper_2201_12931_b200")
+from oracle import cpu_path as O  # noqa: E402
+
+
+def _cantilever(nx, ny, nz):
+    case = O.cantilever_case(nx, ny, nz)
+    grid = vb.build_grid(nx, ny, nz, case.h)
+    loads = [(int(d), float(case.f_ext[d])) for d in np.flatnonzero(case.f_ext)]
+    bnd = vb.make_boundary(grid, np.flatnonzero(case.fixed_mask), loads)
+    return case, grid, vb.Problem(grid, bnd, vb.classify_regions(grid, []))
+
+
+def test_assemble_dense_bit_identical():
+    g = golden("dropin.npz")
+    for tag in "ab":
+        dims = tuple(int(x) for x in g[f"dense_{tag}_dims"])
+        h = float(g[f"dense_{tag}_h"])
+        grid = vb.build_grid(*dims, h)
+        st = vb.OperatorState(grid, g[f"dense_{tag}_rho"], vb.MaterialModel(), g[f"dense_{tag}_fixed"],
+                              vb.unit_stiffness(0.3, h))
+        K = vb.assemble_dense(st)
+        assert np.array_equal(K, g[f"dense_{tag}_K"]), tag
+        with pytest.raises(ValueError, match="guard"):
+            vb.assemble_dense(st, guard=grid.n_dofs - 1)
+
+
+def test_user_preconditioner_pcg_matches_reference():
+    g = golden("dropin.npz")
+    case, grid, _ = _cantilever(16, 8, 8)
+    st = vb.OperatorState(grid, g["up_rho"], vb.MaterialModel(), case.fixed_mask)
+    w = 1.0 / (2.0 * vb.diagonal(st))
+    calls = []
+
+    def prec(r):
+        calls.append(1)
+        return r * w
+
+    l0 = vb.launch_count()
+    x, rep = vb.pcg(st, prec, g["up_f"], cfg=vb.SolverConfig(tolerance=1e-8, max_iterations=3000))
+    assert vb.launch_count() > l0  # the vector algebra ran in libvoxb200
+    want = g["up_rep"]
+    assert rep.converged and rep.iterations == int(want[0])
+    assert rep.precond_applications == int(want[2]) == len(calls)
+    assert rel_err(x, g["up_x"]) <= 1e-8
+    x, rep = vb.pcg(st, prec, g["up_f"], u0=g["up_u0"], cfg=vb.SolverConfig(tolerance=1e-6, max_iterations=60))
+    assert rep.iterations == int(g["upw_rep"][0])
+    assert rel_err(x, g["upw_x"]) <= 1e-8
+
+
+def test_pcg_refuses_duck_typed_state():
+    class Duck:
+        pass
+
+    with pytest.raises(TypeError, match="OperatorState"):
+        vb.pcg(Duck(), None, np.zeros(3))
+
+
+def test_p_continuation_trajectory_matches_reference():
+    g = golden("dropin.npz")
+    case, grid, prob = _cantilever(16, 8, 8)
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=2.5 * grid.h, p=3.0, max_iterations=32, ch_tol=1e-12,
+                       p_continuation=True)
+    res = vb.run(prob, opt, vb.SolverConfig(tolerance=1e-10, max_iterations=1000), scheme="homogenized",
+                 max_levels=3)
+    want = g["pc_recs"]
+    assert len(res.records) == want.shape[0]
+    worst = max(abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(res.records, want))
+    assert worst <= 1e-6, worst
+    assert np.abs(res.densities.values - g["pc_rho32"]).max() <= 1e-4
+
+
+def test_obj_tol_stop_matches_reference():
+    g = golden("dropin.npz")
+    case, grid, prob = _cantilever(16, 8, 8)
+    meta = g["ot_meta"]
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=2.5 * grid.h, max_iterations=40, ch_tol=0.05,
+                       obj_tol=float(meta[2]))
+    res = vb.run(prob, opt, vb.SolverConfig(tolerance=1e-10, max_iterations=1000), scheme="homogenized",
+                 max_levels=3)
+    assert res.iterations == int(meta[0]) and res.converged == bool(meta[1])
+    want = g["ot_recs"]
+    worst = max(abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(res.records, want))
+    assert worst <= 1e-6, worst
+    assert np.abs(res.densities.values - g["ot_rho"]).max() <= 1e-4

@@ -245,3 +245,54 @@ def test_galerkin_trajectory():
     rho, u, recs = O.run_design(case, 0.12, 1.5 * case.h, 20, tol=1e-10, maxit=1000, max_levels=3,
                                 ch_tol=1e-12, scheme="galerkin")
     _check_traj(recs, g["recs_tight"], g["rho20_tight"], rho)
+
+
+# ---------------------------------------------------------------- drop-in surface
+def _dense_case(g, tag):
+    dims = tuple(int(x) for x in g[f"dense_{tag}_dims"])
+    h = float(g[f"dense_{tag}_h"])
+    es = (dims[2], dims[1], dims[0])
+    return dims, h, es
+
+
+def test_dense_assembly_matches_reference():
+    g = golden("dropin.npz")
+    for tag in "ab":
+        dims, h, es = _dense_case(g, tag)
+        K = O.dense_k(es, g[f"dense_{tag}_fixed"], O.hex8_k0(0.3, h), O.simp(g[f"dense_{tag}_rho"], 3.0, 1e-9))
+        assert np.array_equal(K, g[f"dense_{tag}_K"])
+
+
+def test_user_preconditioner_pcg_matches_reference():
+    g = golden("dropin.npz")
+    case = O.cantilever_case(16, 8, 8)
+    fixed = np.flatnonzero(case.fixed_mask)
+    k0 = O.hex8_k0(0.3, case.h)
+    scale = O.simp(g["up_rho"], 3.0, 1e-9)
+    w = 1.0 / (2.0 * O.diag_k(case.es, fixed, k0, scale))
+    ap = lambda p: O.apply_k(p, case.es, fixed, k0, scale)
+    rs = lambda p, ff: O.resid_k(p, ff, case.es, fixed, k0, scale)
+    x, rep = O.pcg(ap, rs, lambda r: r * w, g["up_f"], None, fixed, 1e-8, 3000)
+    assert rep.iterations == int(g["up_rep"][0]) and rep.converged
+    assert rel_err(x, g["up_x"]) <= 1e-9
+    x, rep = O.pcg(ap, rs, lambda r: r * w, g["up_f"], g["up_u0"], fixed, 1e-6, 60)
+    assert rep.iterations == int(g["upw_rep"][0])
+    assert rel_err(x, g["upw_x"]) <= 1e-9
+
+
+def test_p_continuation_and_obj_tol_match_reference():
+    """optimize.py:78-82 (p ramps 1 -> 1.5 -> 2 every 15 iterations) and
+    optimize.py:448-453 (stop needs change <= ch_tol AND |dc| <= obj_tol),
+    with tight solves (1e-10) so the trajectories are rounding-independent."""
+    g = golden("dropin.npz")
+    case = O.cantilever_case(16, 8, 8)
+    rho, _, recs = O.run_design(case, 0.12, 2.5 * case.h, 32, tol=1e-10, maxit=1000, max_levels=3,
+                                ch_tol=1e-12, p_continuation=True)
+    want = g["pc_recs"]
+    assert len(recs) == want.shape[0] == 32
+    assert max(abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(recs, want)) <= 1e-9
+    assert np.abs(rho - g["pc_rho32"]).max() <= 1e-8
+    rho, _, recs = O.run_design(case, 0.12, 2.5 * case.h, 40, tol=1e-10, maxit=1000, max_levels=3,
+                                ch_tol=0.05, obj_tol=float(g["ot_meta"][2]))
+    assert len(recs) == int(g["ot_meta"][0]) == 25
+    assert max(abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(recs, g["ot_recs"])) <= 1e-9
