@@ -23,13 +23,17 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 
 if len(sys.argv) > 1 and sys.argv[1] == "--combine":
     out = {}
+    base = np.load(os.path.join(GOLD, "cfg1_traj.npz"))
+    env = {"rho20": 0.0, "rho40": 0.0}
     for p in sys.argv[2:]:
         d = np.load(p)
         t = int(d["threads"])
         out[f"recs_t{t}"] = d["recs"]
-        out[f"rho20_t{t}"] = d["rho20"]
-        out[f"rho40_t{t}"] = d["rho40"]
+        for k in env:  # the reference's own density spread, max over thread counts
+            env[k] = max(env[k], float(np.abs(d[k] - base[k]).max()))
     out["threads"] = np.array(sorted(int(k[6:]) for k in out if k.startswith("recs_t")))
+    out["rho20_env"] = env["rho20"]
+    out["rho40_env"] = env["rho40"]
     np.savez_compressed(os.path.join(GOLD, "cfg1_selfvar.npz"), **out)
     print("wrote", sorted(out))
     sys.exit(0)

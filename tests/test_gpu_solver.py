@@ -122,22 +122,14 @@ def test_oc_infeasible_raises():
         vb.oc_update(rho, -np.ones(8), np.ones(8), vb.OptConfig(volfrac=0.9, filter_radius=1.0, move=0.1))
 
 
-def _traj_check(res, want, rho_ref, c_tol=1e-4, rho_tol=1e-4, res_tol=1e-5, cg_rel=0.05):
-    """Trajectory bars.  Under the tight protocol (both sides' solves converged
-    to 1e-10, the *_tight tests) the north-star bars hold on every iteration:
-    compliance <= 1e-6 relative (measured ~1e-10), rho <= 1e-4 max-abs.
-
-    At the reference's default tolerance (1e-5) CG in finite precision is
-    chaotic at SIMP contrast: the CUDA kernels agree with the reference to
-    1e-16 per call (operator, V-cycle, coarsest solve: scripts/debug_coarse.py),
-    yet rounding-level differences in the dot products grow ~1e6x in ten CG
-    iterations, so two solves that both stop at a relative residual <= 1e-5
-    differ by that residual's error: |c1 - c2| <= |u| |r1 - r2|, and with a
-    concentrated load |u||f| >> f.u.  The reference does the same against
-    itself across BLAS thread counts (16/40 cfg1 counts differ, DESIGN.md
-    section 4).  At 1e-5 the compliance bar is therefore 10x the solve
-    tolerance (measured worst: 3e-5 on cfg1, at iterations whose CG count moved
-    by one or two)."""
+def _traj_check(res, want, rho_ref, c_tol=1e-6, rho_tol=1e-4, res_tol=1e-5, cg_rel=0.05):
+    """Trajectory bars: compliance <= c_tol relative on every iteration (the
+    north-star 1e-6 by default), rho <= rho_tol max-abs, same volume, residual
+    below the solve tolerance, CG counts within a few percent.  Under the tight
+    protocol (both sides' solves converged to 1e-10, the *_tight tests) the
+    trajectories no longer depend on rounding order (measured ~1e-10).  At the
+    reference default tolerance only cfg1 needs a wider bar, and there it is the
+    reference's own measured spread (test_cfg1_trajectory_parity)."""
     recs = res.records
     assert len(recs) == want.shape[0]
     for r, w in zip(recs, want):
@@ -248,8 +240,24 @@ def test_gravity_trajectory_and_failure():
 @pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "cfg1_traj.npz")), reason="cfg1 fixture missing")
 def test_cfg1_trajectory_parity():
     """BASELINE config 1: 48x24x24 cantilever, p=3, rmin=1.5h, 4-level homogenized MG,
-    40 SIMP iterations; north-star bars: compliance <= 1e-6 rel, rho <= 1e-4 max-abs."""
+    40 SIMP iterations at the reference's default tolerance (1e-5).
+
+    Bar: the north-star 1e-6 compliance / 1e-4 density wherever the reference
+    itself is reproducible to that level, and otherwise the reference's OWN
+    spread: tests/golden/cfg1_selfvar.npz holds the real reference re-run with
+    1, 2, 3, 4 and 8 OpenBLAS threads (8 = the fixture's, bit-identical).  With
+    2 threads the reference moves by 3.2e-5 in compliance at iterations 9-11
+    and 3.6e-5 in density at iteration 20: a solve stopped at a relative
+    residual of 1e-5 does not pin the compliance of those iterations closer
+    than that.  The GPU must stay inside 1.25x that
+    envelope on every iteration."""
     g = golden("cfg1_traj.npz")
+    sv = golden("cfg1_selfvar.npz")
+    want = g["recs"]
+    env_c = max(float(np.max(np.abs(sv[f"recs_t{t}"][:, 1] - want[:, 1]) / np.abs(want[:, 1])))
+                for t in sv["threads"])
+    c_bar = max(1e-6, 1.25 * env_c)
+    rho_bar = max(1e-4, 1.25 * float(sv["rho20_env"]))
     case, grid, prob = _cantilever(48, 24, 24)
     opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * grid.h, p=3.0, max_iterations=40, ch_tol=1e-12)
     seen = {}
@@ -260,16 +268,13 @@ def test_cfg1_trajectory_parity():
 
     res = vb.run(prob, opt, vb.SolverConfig(tolerance=1e-5), scheme="homogenized", max_levels=4,
                  on_iteration=hook)
-    want = g["recs"]
     worst_c = max(abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(res.records, want))
-    worst_eq = max([abs(r.compliance - w[1]) / abs(w[1]) for r, w in zip(res.records, want)
-                    if r.cg_iters == int(w[4])] or [0.0])
     same_its = sum(int(r.cg_iters == int(w[4])) for r, w in zip(res.records, want))
-    print(f"cfg1: worst compliance rel diff {worst_c:.2e} ({worst_eq:.2e} where CG counts agree), "
+    print(f"cfg1: worst compliance rel diff {worst_c:.2e} (reference self-variation envelope {env_c:.2e}), "
           f"equal CG counts {same_its}/40, rho20 {np.abs(seen[20] - g['rho20']).max():.2e}, "
           f"rho40 {np.abs(seen[40] - g['rho40']).max():.2e}")
-    _traj_check(res, want, g["rho40"])
-    assert np.abs(seen[20] - g["rho20"]).max() <= 1e-4
+    _traj_check(res, want, g["rho40"], c_tol=c_bar, rho_tol=rho_bar)
+    assert np.abs(seen[20] - g["rho20"]).max() <= rho_bar
 
 
 def test_pcg_graph_not_reused_across_hierarchies():
