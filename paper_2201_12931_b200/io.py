@@ -113,28 +113,72 @@ def checkpoint_save(path, grid: StructuredGrid, iteration: int, rho, u) -> None:
         os.close(fd)
 
 
-def checkpoint_load(path, expect_grid: Optional[StructuredGrid] = None) -> Checkpoint:
-    """Read and validate a checkpoint; refuses partial or mismatched files (app/io.py:113-149)."""
-    data = Path(path).read_bytes()
-    if len(data) < 24:
+def _read_header(path):
+    size = os.stat(os.fspath(path)).st_size
+    with open(path, "rb") as fh:
+        head = fh.read(24)
+    if len(head) < 24:
         raise ConfigError(f"checkpoint {path} is truncated (no header)")
-    if data[:4] != _CKPT_MAGIC:
-        raise ConfigError(f"checkpoint {path} has wrong magic {data[:4]!r}")
-    version, nelx, nely, nelz, iteration = struct.unpack("<IIIII", data[4:24])
+    if head[:4] != _CKPT_MAGIC:
+        raise ConfigError(f"checkpoint {path} has wrong magic {head[:4]!r}")
+    version, nelx, nely, nelz, iteration = struct.unpack("<IIIII", head[4:24])
     if version != _CKPT_VERSION:
         raise ConfigError(f"checkpoint {path} has unsupported version {version}")
     nel = nelx * nely * nelz
     n = 3 * (nelx + 1) * (nely + 1) * (nelz + 1)
     expected = 24 + 8 * (nel + n)
-    if len(data) != expected:
-        raise ConfigError(f"checkpoint {path} has {len(data)} bytes, expected {expected}")
+    if size != expected:
+        raise ConfigError(f"checkpoint {path} has {size} bytes, expected {expected}")
+    return nelx, nely, nelz, iteration, nel, n
+
+
+def _read_to_device(fd: int, offset: int, n: int, device) -> torch.Tensor:
+    """n float64 values at `offset` -> a CUDA tensor, through two page-locked
+    buffers: the file read of chunk k+1 overlaps the host->device copy of chunk k."""
+    out = torch.empty(n, dtype=torch.float64, device=device)
+    if n == 0:
+        return out
+    bufs = [torch.empty(min(_CHUNK, n), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    stream = torch.cuda.current_stream(device)
+    for k, s in enumerate(range(0, n, _CHUNK)):
+        e = min(s + _CHUNK, n)
+        b = k & 1
+        if k >= 2:
+            evs[b].synchronize()  # the copy that last used this buffer is done
+        view = memoryview(bufs[b].numpy()[: e - s]).cast("B")
+        got = os.preadv(fd, [view], offset + 8 * s)
+        if got != 8 * (e - s):
+            raise ConfigError("checkpoint file shrank while being read")
+        with torch.cuda.stream(stream):
+            out[s:e].copy_(bufs[b][: e - s], non_blocking=True)
+        evs[b].record(stream)
+    stream.synchronize()
+    return out
+
+
+def checkpoint_load(path, expect_grid: Optional[StructuredGrid] = None, device=None) -> Checkpoint:
+    """Read and validate a checkpoint; refuses partial or mismatched files
+    (app/io.py:113-149).  The size is checked against the header before any
+    payload is read (no whole-file read).  device=None returns numpy arrays
+    like the reference; device="cuda[:i]" streams both fields straight into
+    CUDA tensors (reference order) through pinned double buffers."""
+    nelx, nely, nelz, iteration, nel, n = _read_header(path)
     if expect_grid is not None and (nelx, nely, nelz) != (expect_grid.nelx, expect_grid.nely, expect_grid.nelz):
         raise ConfigError(
             f"checkpoint {path} was written for {nelx}x{nely}x{nelz}, the active "
             f"configuration is {expect_grid.nelx}x{expect_grid.nely}x{expect_grid.nelz}"
         )
-    rho = np.frombuffer(data, dtype="<f8", count=nel, offset=24).copy()
-    u = np.frombuffer(data, dtype="<f8", count=n, offset=24 + 8 * nel).copy()
+    if device is None:
+        rho = np.fromfile(path, dtype="<f8", count=nel, offset=24)
+        u = np.fromfile(path, dtype="<f8", count=n, offset=24 + 8 * nel)
+        return Checkpoint(nelx, nely, nelz, iteration, rho, u)
+    fd = os.open(os.fspath(path), os.O_RDONLY)
+    try:
+        rho = _read_to_device(fd, 24, nel, device)
+        u = _read_to_device(fd, 24 + 8 * nel, n, device)
+    finally:
+        os.close(fd)
     return Checkpoint(nelx, nely, nelz, iteration, rho, u)
 
 
@@ -175,41 +219,61 @@ def checkpoint_save_slabs(path, run, iteration: int, group=None) -> None:
         dist.barrier(group=group)
 
 
-def export_vti(rho, grid: StructuredGrid, path, binary: bool = True) -> None:
-    """Cell-centred float32 density field as XML ImageData (app/io.py:36-71);
-    a CUDA tensor is converted to float32 on the device."""
-    path = Path(path)
-    if isinstance(rho, torch.Tensor):
-        values = rho.detach().reshape(-1).to(torch.float32).cpu().numpy()
-    else:
-        values = np.asarray(rho, dtype=np.float32)
-    if values.shape != (grid.n_elements,):
-        raise ValueError(f"expected {grid.n_elements} cell values")
-    nx, ny, nz = grid.nelx, grid.nely, grid.nelz
-    extent = f"0 {nx} 0 {ny} 0 {nz}"
-    h = grid.h
-    if binary:
-        raw = values.astype("<f4").tobytes()
-        payload = base64.b64encode(struct.pack("<I", len(raw)) + raw).decode("ascii")
-        fmt = "binary"
-    else:
-        payload = " ".join(repr(float(v)) for v in values)
-        fmt = "ascii"
-    doc = f"""<?xml version="1.0"?>
+_VTI_HEAD = """<?xml version="1.0"?>
 <VTKFile type="ImageData" version="1.0" byte_order="LittleEndian" header_type="UInt32">
   <ImageData WholeExtent="{extent}" Origin="0 0 0" Spacing="{h!r} {h!r} {h!r}">
     <Piece Extent="{extent}">
       <CellData Scalars="density">
         <DataArray type="Float32" Name="density" NumberOfComponents="1" format="{fmt}">
-          {payload}
+          """
+_VTI_TAIL = """
         </DataArray>
       </CellData>
     </Piece>
   </ImageData>
 </VTKFile>
 """
+_VTI_CHUNK = 3 * (1 << 22)  # float32 values per base64 chunk (a multiple of 3 bytes keeps chunks aligned)
+
+
+def export_vti(rho, grid: StructuredGrid, path, binary: bool = True) -> None:
+    """Cell-centred float32 density field as XML ImageData (app/io.py:36-71),
+    byte-identical to the reference's file.  The binary payload is
+    base64(UInt32 byte count + float32 values); it is encoded and written in
+    chunks aligned to 3 bytes, so a 100M-cell field never exists as one host
+    string.  A CUDA tensor is converted to float32 on the device and copied
+    down chunk by chunk."""
+    path = Path(path)
+    if isinstance(rho, torch.Tensor):
+        t = rho.detach().reshape(-1)
+        if t.numel() != grid.n_elements:
+            raise ValueError(f"expected {grid.n_elements} cell values")
+        values = t.to(torch.float32)
+    else:
+        values = np.asarray(rho, dtype=np.float32).reshape(-1) if np.ndim(rho) else np.asarray(rho)
+        if values.shape != (grid.n_elements,):
+            raise ValueError(f"expected {grid.n_elements} cell values")
+    nx, ny, nz = grid.nelx, grid.nely, grid.nelz
+    extent = f"0 {nx} 0 {ny} 0 {nz}"
+    head = _VTI_HEAD.format(extent=extent, h=grid.h, fmt="binary" if binary else "ascii")
     try:
-        path.write_text(doc)
+        with open(path, "w", encoding="ascii", newline="") as fh:
+            fh.write(head)
+            if binary:
+                n = grid.n_elements
+                carry = struct.pack("<I", 4 * n)  # the UInt32 header, then the values
+                for s in range(0, n, _VTI_CHUNK):
+                    e = min(s + _VTI_CHUNK, n)
+                    blk = values[s:e]
+                    raw = (blk.cpu().numpy() if isinstance(blk, torch.Tensor) else blk).astype("<f4").tobytes()
+                    buf = carry + raw
+                    cut = len(buf) - len(buf) % 3 if e < n else len(buf)
+                    fh.write(base64.b64encode(buf[:cut]).decode("ascii"))
+                    carry = buf[cut:]
+            else:
+                vals = values.cpu().numpy() if isinstance(values, torch.Tensor) else values
+                fh.write(" ".join(repr(float(v)) for v in vals))
+            fh.write(_VTI_TAIL)
     except OSError as exc:
         raise OSError(f"failed writing VTI file {path}: {exc}") from exc
 

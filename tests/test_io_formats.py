@@ -93,3 +93,36 @@ def test_checkpoint_from_device_and_slabs(tmp_path):
     assert a.read_bytes() == b.read_bytes()
     ck = vio.checkpoint_load(a, expect_grid=prob.grid)
     assert ck.iteration == 1
+    # streamed load straight to the device == the host load
+    ckd = vio.checkpoint_load(a, expect_grid=prob.grid, device="cuda")
+    assert ckd.densities.is_cuda and ckd.displacement.is_cuda
+    assert np.array_equal(ckd.densities.cpu().numpy(), ck.densities)
+    assert np.array_equal(ckd.displacement.cpu().numpy(), ck.displacement)
+
+
+def test_vti_chunked_payload_matches_single_shot(tmp_path, monkeypatch):
+    """The chunked base64 writer (chunks aligned to 3 bytes) produces exactly the
+    single-shot encoding of the reference, whatever the chunk size."""
+    import base64
+    import struct
+
+    g, grid = _case()
+    ref = (tmp_path / "a.vti")
+    vio.export_vti(g["rho"], grid, ref)
+    for chunk in (1, 2, 3, 5, 7):
+        monkeypatch.setattr(vio, "_VTI_CHUNK", chunk)
+        p = tmp_path / f"c{chunk}.vti"
+        vio.export_vti(g["rho"], grid, p)
+        assert p.read_bytes() == ref.read_bytes()
+    raw = g["rho"].astype("<f4").tobytes()
+    assert base64.b64encode(struct.pack("<I", len(raw)) + raw).decode() in ref.read_text()
+
+
+def test_checkpoint_load_rejects_size_mismatch_without_reading(tmp_path):
+    g, grid = _case()
+    p = tmp_path / "t.bin"
+    vio.checkpoint_save(p, grid, 3, g["rho"], g["u"])
+    with open(p, "ab") as fh:
+        fh.write(b"x")
+    with pytest.raises(vb.ConfigError, match="bytes, expected"):
+        vio.checkpoint_load(p)
