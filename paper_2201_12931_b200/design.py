@@ -255,9 +255,10 @@ def oc_update(rho: DensityField, dc, dv, cfg: OptConfig) -> OcResult:
     flat = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
     rt = flat(rho.values)
     ct = torch.as_tensor(np.ascontiguousarray(rho.regions.classes, dtype=np.int8), device=dev)
+    dct, dvt = flat(dc), flat(dva)  # keep the device copies alive across the call
     out = torch.empty_like(rt)
     lam, steps = C.c_double(), C.c_int()
-    check(lib.vt_oc_update_flat(nel, ptr(rt), ptr(ct), ptr(flat(dc)), ptr(flat(dva)), float(cfg.volfrac),
+    check(lib.vt_oc_update_flat(nel, ptr(rt), ptr(ct), ptr(dct), ptr(dvt), float(cfg.volfrac),
                                 float(cfg.move), float(cfg.eta), float(cfg.q), ptr(out), C.byref(lam),
                                 C.byref(steps), stream_ptr()))
     lam, steps = lam.value, steps.value
