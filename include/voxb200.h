@@ -125,7 +125,8 @@ vt_status vt_axpy(vt_grid *g, int mode, double a, const double *x, double *y, vo
 vt_status vt_project(vt_grid *g, const double *src, double *dst, void *stream);
 /* K (n x n, device, n = n_dofs) = the dense global stiffness with identity
  * rows / columns on fixed dofs, bit-identical to the reference's np.add.at
- * assembly [ref: operator.py:187-205]; k0: 576 device doubles.  The caller
+ * assembly [ref: operator.py:187-205]; scale: plain (n_elements,) device
+ * array in the reference element order, k0: 576 device doubles.  The caller
  * enforces the reference's dense guard. */
 vt_status vt_assemble_dense(vt_grid *g, const double *scale, const double *k0, double *K,
                             void *stream);

@@ -139,6 +139,7 @@ vt_status launch_axpy(vt_grid* G, int mode, double a, const double* x, double* y
 // Dense global stiffness with identity rows / columns on fixed dofs
 // [ref: operator.py:187-205].  One CTA of 576 threads walks the elements in the
 // reference's order; thread (a, b) adds s_e K0[a][b] into K[dof_a][dof_b].
+// `scale` is plain (n_elements,) in the reference element order.
 // An element's 24 dofs are distinct, so its 576 targets are too, and the
 // barrier per element makes every entry accumulate in ascending element order
 // -- the order of np.add.at -- so K is bit-identical to the reference's.
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(576, 1)
   const int nel = g.nx * g.ny * (g.k1 - g.k0);
   for (int e = 0; e < nel; ++e) {
     const int i = e % g.nx, j = (e / g.nx) % g.ny, k = e / (g.nx * g.ny);
-    const double s = scale[elem_off(g, k + 1, j, i)];
+    const double s = scale[e];
     const long long na = (i + (ca & 1)) + (long long)(j + ((ca >> 1) & 1)) * nx1 + (long long)(k + (ca >> 2)) * nx1 * ny1;
     const long long nb = (i + (cb & 1)) + (long long)(j + ((cb >> 1) & 1)) * nx1 + (long long)(k + (cb >> 2)) * nx1 * ny1;
     double* dst = K + (3 * na + a % 3) * n + 3 * nb + b % 3;

@@ -167,15 +167,19 @@ def residual(state: OperatorState, u, f):
 def assemble_dense(state: OperatorState, guard: int = DENSE_GUARD_DOFS) -> np.ndarray:
     """Explicit global stiffness with identity rows/columns on fixed dofs
     (operator.py:187-205).  Assembled on the device in the reference's
-    element order, so the result is bit-identical to its np.add.at sum;
-    refuses grids above the guard limit like the reference."""
+    element order from the reference's scale E*s(rho) (numpy's pow, as
+    operator.py:142 evaluates it), so the result is bit-identical to its
+    np.add.at sum; refuses grids above the guard limit like the reference."""
+    from .material import simp_scale
+
     n = state.grid.n_dofs
     if n > guard:
         raise ValueError(f"dense assembly of {n} dofs exceeds the guard limit {guard}")
     d = state.dgrid
+    sc = torch.as_tensor(state.model.E * simp_scale(state.densities, state.model), device=f"cuda:{d.device}")
     k0 = torch.as_tensor(np.ascontiguousarray(state.stiffness.matrix, dtype=np.float64).reshape(-1),
                          device=f"cuda:{d.device}")
     K = torch.empty((n, n), dtype=torch.float64, device=f"cuda:{d.device}")
-    check(lib.vt_assemble_dense(d.handle, ptr(state.scale_dev), ptr(k0), ptr(K), stream_ptr()),
+    check(lib.vt_assemble_dense(d.handle, ptr(sc), ptr(k0), ptr(K), stream_ptr()),
           "vt_assemble_dense")
     return K.cpu().numpy()
