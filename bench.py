@@ -51,7 +51,9 @@ def _args():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 single-GPU section")
     ap.add_argument("--slabs", action="store_true",
-                    help="use the z-slab/NCCL path even at N=1 (under torchrun; smoke test of the transport)")
+                    help="use the z-slab path even at N=1 (under torchrun; smoke test of the transport)")
+    ap.add_argument("--transport", default=os.environ.get("VT_TRANSPORT", "peer"), choices=["peer", "nccl"],
+                    help="slab exchange: peer = one kernel per exchange over CUDA IPC / NVLink, nccl = NCCL")
     return ap.parse_args()
 
 
@@ -182,10 +184,18 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # VT_BENCH_SHARE_GPU=1: every rank on cuda:0 with a gloo group -- a smoke
+    # test of the multi-process path on a one-GPU box (timings not meaningful)
+    share = os.environ.get("VT_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     slabs = world > 1 or a.slabs
     if slabs:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if slabs:
@@ -195,7 +205,7 @@ def run_ours(a):
     def max_over_ranks(x):
         if not slabs:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -238,7 +248,7 @@ def run_ours(a):
         # one slab per rank, NCCL halo planes before every apply
         from paper_2201_12931_b200.slabs import SlabSolver
 
-        S = SlabSolver.from_process_group(grid, fm, levels=spec["levels"])
+        S = SlabSolver.from_process_group(grid, fm, levels=spec["levels"], transport=a.transport)
         S.set_density(rho, problem.model)
         us = S.upload(u_host)
         vs = S.zeros()
@@ -254,7 +264,7 @@ def run_ours(a):
         def e2e_step():
             return S.download(S.apply(S.upload(u_np)))
 
-        parallelism = f"{world} z-slabs (NCCL halo planes), layers {list(S.plan.bounds)}"
+        parallelism = (f"{world} z-slabs ({a.transport} halo planes), layers {list(S.plan.bounds)}")
         scaling = "strong"
 
     for _ in range(max(a.warmup, 3)):
@@ -324,7 +334,8 @@ def run_ours(a):
         from paper_2201_12931_b200.slabs import SlabRun
 
         opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
-        R = SlabRun.from_process_group(problem, opt, vb.SolverConfig(tolerance=1e-5), spec["levels"], 0.4)
+        R = SlabRun.from_process_group(problem, opt, vb.SolverConfig(tolerance=1e-5), spec["levels"], 0.4,
+                                       transport=a.transport)
         times, its = [], []
         for it in range(a.simp_iters):
             barrier()
@@ -359,7 +370,7 @@ def run_ours(a):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
-                     "kernel": "hex8_tile_kernel<APPLY> (+ NCCL halo planes when N > 1)"},
+                     "kernel": "hex8_tile_kernel<APPLY> (+ the halo-plane exchange when N > 1)"},
         "e2e": {"value": n / t_e2e / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n,
                 "path": "paper_2201_12931_b200.apply(state, pinned numpy) -> numpy (vt_apply_host, "
