@@ -90,7 +90,7 @@ def _run(dims, gravity=None, iters=3, world=2):
     return next(o for o in out if o[1] is not None)
 
 
-@pytest.mark.parametrize("dims", [(16, 8, 16), (8, 8, 32)])
+@pytest.mark.parametrize("dims", [(16, 8, 16), (8, 8, 32)], ids=["a", "b"])
 def test_two_process_run_bit_identical_to_in_process_slabs(dims):
     _, (recs, rho, u), (rrecs, rrho, ru), _ = _run(dims)
     assert recs == rrecs

@@ -308,3 +308,12 @@ def test_reference_self_variation_fixture():
     assert np.array_equal(sv["recs_t8"], base)
     d2 = np.abs(sv["recs_t2"][:, 1] - base[:, 1]) / np.abs(base[:, 1])
     assert d2.max() > 1e-5 and int(np.argmax(d2)) + 1 in (9, 10, 11)
+
+
+def test_reference_self_variation_small_fixture():
+    """tests/golden/selfvar_small.npz (oracle/ref_self_variation_small.py): the
+    8-thread re-runs reproduce the small / bridge / self-weight fixtures bit for
+    bit; the other thread counts give the reference's own spread."""
+    sv = golden("selfvar_small.npz")
+    for c in ("small", "bridge", "grav"):
+        assert np.array_equal(sv[f"{c}_t8"], golden(f"{c}_traj.npz")["recs"])
