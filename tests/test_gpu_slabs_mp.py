@@ -43,7 +43,8 @@ def _summary(res):
 
 
 def _worker(rank, world, port, dims, gravity, iters, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), VT_PEER_TIMEOUT_S="120")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.setdefault("VT_PEER_TIMEOUT_S", "120")
     import torch.distributed as dist
 
     torch.cuda.set_device(0)
