@@ -429,7 +429,10 @@ static int tail_cluster_size(int smem) {
     cudaGetLastError();
     return g_tail_cluster;
   }
-  for (int cs : {16, 8, 4}) {
+  const char* force = getenv("VT_TAIL_CLUSTER");  // dev: force a cluster size
+  const int sizes_all[3] = {16, 8, 4};
+  for (int cs : sizes_all) {
+    if (force && atoi(force) > 0 && cs != atoi(force)) continue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(TAIL_THREADS);
