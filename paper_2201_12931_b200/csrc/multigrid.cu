@@ -738,10 +738,7 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
     ucur[l] = dst;
     return VT_OK;
   };
-  // levels >= T run as one cluster launch (tail.cu); T = L - 1: no tail
-  const int T0 = tail_start(H, top);
-  const int T = T0 < 0 ? L - 1 : T0;
-  for (int l = top; l < T; ++l) {
+  for (int l = top; l < L - 1; ++l) {
     vt_grid* G = H->lv[l];
     ucur[l] = H->u[l];
     if (H->sweeps >= 1) {
@@ -761,14 +758,9 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
       VT_TRY(launch_restrict(G, H->lv[l + 1], fl[l], H->f[l + 1], stop, -1, -1, s));
     }
   }
-  if (T0 >= 0) {
-    VT_TRY(launch_tail_vcycle(H, T, fl[T], stop, s));
-    ucur[T] = H->u[T];
-  } else {
-    VT_TRY(launch_coarse_solve(H, fl[L - 1], H->u[L - 1], stop, s));
-    ucur[L - 1] = H->u[L - 1];
-  }
-  for (int l = T - 1; l >= top; --l) {
+  VT_TRY(launch_coarse_solve(H, fl[L - 1], H->u[L - 1], stop, s));
+  ucur[L - 1] = H->u[L - 1];
+  for (int l = L - 2; l >= top; --l) {
     vt_grid* G = H->lv[l];
     VT_TRY(launch_prolong_add(H->lv[l + 1], G, ucur[l + 1], ucur[l], stop, s));
     for (int k = 0; k < H->sweeps; ++k) VT_TRY(smooth(l, want_rz && l == 0 && k == H->sweeps - 1));
@@ -856,9 +848,6 @@ vt_status vt_hier_create_ex(vt_hier** out, vt_grid* fine, int n_levels, double o
     cudaDeviceSynchronize();  // coarse masks are built on the legacy stream
     vt_status st = gal_setup(H);
     if (st != VT_OK) { vt_hier_destroy(H); return st; }
-  } else {
-    vt_status st = tail_alloc(H);
-    if (st != VT_OK) { vt_hier_destroy(H); return st; }
   }
   *out = H;
   return VT_OK;
@@ -874,7 +863,6 @@ vt_status vt_hier_destroy(vt_hier* H) {
     if (l > 0) vt_grid_destroy(H->lv[l]);
   }
   gal_free(H);
-  cudaFree(H->tail_ev);
   cudaFree(H->A); cudaFree(H->A0); cudaFree(H->cvec); cudaFree(H->W); cudaFree(H->Kinv); cudaFree(H->k0l); cudaFree(H->status);
   delete H;
   return VT_OK;

@@ -143,19 +143,9 @@ struct vt_hier {
   bool gal_mf = false;              // level 1 applied matrix-free (P^T K0 P)
   bool mats1_fresh = false;         // mats[1] materialized for the current refresh
   double *gfa = nullptr, *gfb = nullptr, *gc1 = nullptr;  // fine x2 / level-1 scratch
-  // one-launch coarse tail (tail.cu): first level and element scratch
-  int tail_T = -1;
-  double* tail_ev = nullptr;
 };
 
 namespace vt {
-// one-launch coarse tail of the homogenized V-cycle (tail.cu)
-constexpr long long TAIL_MAX_EL = 32768;  // first tail level: at most this many elements
-constexpr int TAIL_MAX_NL = 2048;         // coarsest dofs the tail's mat-vec stages in smem
-vt_status tail_alloc(vt_hier* H);
-int tail_start(vt_hier* H, int top);
-vt_status launch_tail_vcycle(vt_hier* H, int T, const double* fT, const int* stop, cudaStream_t s);
-
 // TMA descriptors (cached per device pointer)
 const CUtensorMap* vec_map(vt_grid* G, const void* ptr);
 const CUtensorMap* elem_map(vt_grid* G, const void* ptr);
