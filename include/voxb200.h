@@ -279,6 +279,13 @@ int vt_peer_handle_bytes(void);
 vt_status vt_dist_peer_handle(vt_dist *D, uint8_t *out, int nbytes);
 vt_status vt_dist_peer_open(vt_dist *D, const uint8_t *handles, int nbytes);
 vt_status vt_dist_destroy(vt_dist *D);
+/* Switch to the reference's default Galerkin scheme [ref: multigrid.py:216-278]
+ * before the first refresh (dist_level must be 1): levels 0 and 1 stay on the
+ * slabs (level 1 matrix-free through the fine kernels), the stored-matrix
+ * levels >= 2 and the coarsest solve run replicated, built each refresh from
+ * the gathered fine scale field (csrc/dist_galerkin.cu). */
+vt_status vt_dist_set_scheme(vt_dist *D, int scheme);
+int vt_dist_scheme(const vt_dist *D);
 int vt_dist_levels(const vt_dist *D);
 int vt_dist_dist_level(const vt_dist *D);
 int vt_dist_nlocal(const vt_dist *D);

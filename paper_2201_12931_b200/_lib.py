@@ -93,6 +93,8 @@ _SIGS = {
     "vt_nccl_id_bytes": (I, []),
     "vt_nccl_unique_id": (I, [P, I]),
     "vt_dist_create": (I, [C.POINTER(P), I, I, I, D, D, P, I, D, I, I, I, P, I, P, I]),
+    "vt_dist_set_scheme": (I, [P, I]),
+    "vt_dist_scheme": (I, [P]),
     "vt_dist_create_peer": (I, [C.POINTER(P), I, I, I, D, D, P, I, D, I, I, P, I, I]),
     "vt_peer_handle_bytes": (I, []),
     "vt_dist_peer_handle": (I, [P, P, I]),

@@ -212,11 +212,10 @@ vt_status host_slot_values(vt_dist* D, int slot, cudaStream_t s, double* out) {
   return peer_check(D);
 }
 
-// tail-level rhs ranges written by each rank -> every rank
-static vt_status gather_tail_f(vt_dist* D, cudaStream_t s) {
+// tail-level rhs ranges written by each rank -> every rank (C / f: the
+// replicated grid of level D+1 and its rhs)
+vt_status gather_tail_f(vt_dist* D, vt_grid* C, double* f, cudaStream_t s) {
   if (!D->remote()) return VT_OK;
-  vt_grid* C = D->tail->lv[1];
-  double* f = D->tail->f[1];
   auto range = [&](int r, int* kb, int* ke) {
     const int a = lvl_k(D->kb[r], D->D), b = lvl_k(D->kb[r + 1], D->D) + (r == D->N - 1 ? 1 : 0);
     *kb = (a + 1) / 2;
@@ -253,6 +252,7 @@ static vt_status gather_tail_f(vt_dist* D, cudaStream_t s) {
 // smoother land in each slab's partial + 3*4096.  Capturable.
 static vt_status dist_vcycle(vt_dist* D, const std::vector<const double*>& f0, const int* stop,
                              bool want_rz, cudaStream_t s) {
+  if (D->scheme == 1) return dist_vcycle_galerkin(D, f0, stop, want_rz, s);
   const int NL = (int)D->sl.size();
   const int Dl = D->D;
   std::vector<std::vector<double*>> ucur(Dl + 1, std::vector<double*>(NL));
@@ -284,7 +284,7 @@ static vt_status dist_vcycle(vt_dist* D, const std::vector<const double*>& f0, c
       }
     }
   }
-  VT_TRY(gather_tail_f(D, s));
+  VT_TRY(gather_tail_f(D, D->tail->lv[1], D->tail->f[1], s));
   const double* zt = nullptr;
   VT_TRY(hier_vcycle_launch(D->tail, D->tail->f[1], stop, nullptr, false, s, &zt, 1));
   for (int l = Dl; l >= 0; --l) {
@@ -458,6 +458,9 @@ static vt_status dist_create(vt_dist** out, int nx, int ny, int nz, double h, do
   D->N = nranks; D->rank0 = rank0; D->nlocal = nlocal; D->L = levels; D->D = dist_level;
   D->device = device; D->omega = omega; D->nx = nx; D->ny = ny; D->nz = nz;
   D->kb.assign(kbounds, kbounds + nranks + 1);
+  D->h = h;
+  D->nu = nu;
+  D->node_mask.assign(node_mask, node_mask + (size_t)(nx + 1) * (ny + 1) * (nz + 1));
   vt_status st = VT_OK;
   auto bail = [&](vt_status s2) { vt_dist_destroy(D); return s2; };
   if (nccl_id) {
@@ -604,6 +607,7 @@ vt_status vt_dist_destroy(vt_dist* D) {
   for (double* p : D->fprod) cudaFree(p);
   for (double* p : D->gpad) cudaFree(p);
   if (D->comm) nccl().CommDestroy(D->comm);
+  dist_galerkin_free(D);
   peer_free(D);
   delete D;
   return VT_OK;
@@ -641,6 +645,11 @@ vt_status vt_dist_refresh(vt_dist* D, const double* const* rho, const double* co
   cudaStream_t s = (cudaStream_t)stream;
   VT_CUDA(cudaSetDevice(D->device));
   VT_TRY(vt_dist_set_scale(D, scale0, stream));
+  if (D->scheme == 1) {
+    VT_TRY(dist_refresh_galerkin(D, p, kmin, E, s));
+    D->refreshed = true;
+    return VT_OK;
+  }
   int* bad = reinterpret_cast<int*>(D->sl[0].lv[0]->scalars);
   VT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   for (int i = 0; i < D->nlocal; ++i) {

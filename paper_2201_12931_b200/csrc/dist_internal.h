@@ -120,6 +120,13 @@ struct vt_dist {
   std::vector<double*> gpad;            // per slab: rho with the element layer below (gravity)
 
   vt::PeerXport* px = nullptr;         // peer-memory transport (peer.cu), else NCCL when comm
+  // Galerkin scheme on slabs (dist_galerkin.cu)
+  int scheme = 0;                      // 0 homogenized, 1 galerkin (needs dist level 1)
+  double h = 0.0, nu = 0.3;
+  std::vector<uint8_t> node_mask;      // host copy of the fine fixed mask (whole grid)
+  vt_grid* gfine = nullptr;            // the whole fine grid (replicated)
+  vt_hier* gtail = nullptr;            // whole Galerkin hierarchy; its levels >= 2 are the tail
+  std::vector<double*> gfa, gfb, gc1, gd1;  // per slab: level-0 / level-1 scratch, level-1 diagonal
 
   bool remote() const { return comm != nullptr || px != nullptr; }
 };
@@ -141,6 +148,11 @@ vt_status slab_sum(vt_dist* D, int i, const double* partial, int n, int n50, int
                    const PcgCtl* ctl, cudaStream_t s);
 vt_status host_slot_sum(vt_dist* D, int slot, cudaStream_t s, double* out);
 vt_status host_slot_values(vt_dist* D, int slot, cudaStream_t s, double* out);
+vt_status gather_tail_f(vt_dist* D, vt_grid* C, double* f, cudaStream_t s);
+vt_status dist_vcycle_galerkin(vt_dist* D, const std::vector<const double*>& f0, const int* stop,
+                               bool want_rz, cudaStream_t s);
+vt_status dist_refresh_galerkin(vt_dist* D, double p, double kmin, double E, cudaStream_t s);
+void dist_galerkin_free(vt_dist* D);
 vt_status peer_init(vt_dist* D, size_t stage_doubles);
 void peer_free(vt_dist* D);
 vt_status peer_check(vt_dist* D);

@@ -570,6 +570,30 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
   return VT_OK;
 }
 
+// the same passes on a grid that is not a hierarchy level (a z-slab of level 1)
+vt_status launch_gal_jacobi0(vt_grid* G, const double* f, const double* d, double omega, double* u,
+                             const int* stop, cudaStream_t s) {
+  launch_pdl(gal_jacobi0_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * (G->g.ny + 1) * (G->g.nx + 1), GL_THREADS, G->nsm * 4), GL_THREADS, 0, s, G->g, G->mask, f, d, omega, u, stop);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
+vt_status launch_gal_vec_epilogue(vt_grid* G, int mode, const double* v, const double* u, const double* f,
+                                  const double* d, double omega, double* out, const int* stop,
+                                  cudaStream_t s) {
+  const int grid_n = fit_grid((long long)(G->g.pB - G->g.pA) * (G->g.ny + 1) * (G->g.nx + 1), GL_THREADS, G->nsm * 4);
+  if (mode == 0)
+    launch_pdl(gal_vec_epilogue_kernel<0>, grid_n, GL_THREADS, 0, s, G->g, G->mask, v, u, f, d, omega, out, stop);
+  else if (mode == 1)
+    launch_pdl(gal_vec_epilogue_kernel<1>, grid_n, GL_THREADS, 0, s, G->g, G->mask, v, u, f, d, omega, out, stop);
+  else
+    launch_pdl(gal_vec_epilogue_kernel<2>, grid_n, GL_THREADS, 0, s, G->g, G->mask, v, u, f, d, omega, out, stop);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
+}
+
 vt_status gal_jacobi0(vt_hier* H, int l, const double* f, double* u, const int* stop, cudaStream_t s) {
   vt_grid* G = H->lv[l];
   launch_pdl(gal_jacobi0_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * (G->g.ny + 1) * (G->g.nx + 1), GL_THREADS, G->nsm * 4), GL_THREADS, 0, s, G->g, G->mask, f, H->gdiag[l], H->omega, u, stop);

@@ -893,6 +893,17 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
                           cudaMemcpyDeviceToDevice, s));
   VT_CUDA(cudaMemcpyAsync(H->rho[0], rho, F->nel_local() * sizeof(double),
                           cudaMemcpyDeviceToDevice, s));
+  return hier_refresh_levels(H, p, kmin, E, s);
+}
+
+}  // extern "C"
+
+namespace vt {
+// everything of a refresh after the level-0 scale (and densities) are in
+// place: coarse operators, damped inverse diagonals, the coarsest factor
+vt_status hier_refresh_levels(vt_hier* H, double p, double kmin, double E, cudaStream_t s) {
+  const int L = (int)H->lv.size();
+  vt_grid* F = H->lv[0];
   int* bad = reinterpret_cast<int*>(F->scalars);
   VT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   if (H->scheme == 1) {
@@ -972,6 +983,9 @@ vt_status vt_hier_refresh(vt_hier* H, const double* rho, const double* scale0, d
   H->factored = true;
   return VT_OK;
 }
+}  // namespace vt
+
+extern "C" {
 
 vt_status vt_hier_vcycle(vt_hier* H, const double* f, double* z, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;

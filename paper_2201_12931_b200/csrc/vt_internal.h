@@ -146,6 +146,7 @@ struct vt_hier {
 };
 
 namespace vt {
+vt_status hier_refresh_levels(vt_hier* H, double p, double kmin, double E, cudaStream_t s);
 // TMA descriptors (cached per device pointer)
 const CUtensorMap* vec_map(vt_grid* G, const void* ptr);
 const CUtensorMap* elem_map(vt_grid* G, const void* ptr);
@@ -195,6 +196,11 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
                        const int* stop, cudaStream_t s);
 vt_status gal_jacobi0(vt_hier* H, int l, const double* f, double* u, const int* stop, cudaStream_t s);
 vt_status gal_materialize_level1(vt_hier* H, cudaStream_t s);
+vt_status launch_gal_jacobi0(vt_grid* G, const double* f, const double* d, double omega, double* u,
+                             const int* stop, cudaStream_t s);
+vt_status launch_gal_vec_epilogue(vt_grid* G, int mode, const double* v, const double* u, const double* f,
+                                  const double* d, double omega, double* out, const int* stop,
+                                  cudaStream_t s);
 vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
                              cudaStream_t s);
 }  // namespace vt

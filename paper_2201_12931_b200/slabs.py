@@ -79,19 +79,22 @@ class SlabPlan:
         return ops
 
 
-def plan_slabs(nz: int, levels: int, nranks: int) -> SlabPlan:
+def plan_slabs(nz: int, levels: int, nranks: int, max_dist_level: Optional[int] = None) -> SlabPlan:
     """Even z-slabs whose boundaries survive the deepest possible coarsening.
 
-    D = the largest level d <= levels-2 at which nz / 2**d layers split evenly
-    into nranks slabs (so every distributed level is balanced and every slab
-    boundary falls on an even coarse layer); levels d+1.. are replicated."""
+    D = the largest level d <= levels-2 (and <= max_dist_level) at which
+    nz / 2**d layers split evenly into nranks slabs (so every distributed level
+    is balanced and every slab boundary falls on an even coarse layer); levels
+    d+1.. are replicated.  The Galerkin scheme distributes exactly levels 0 and
+    1 (max_dist_level=1, and D must reach 1)."""
     if nranks < 1:
         raise ValueError("nranks must be positive")
     if levels < 2:
         raise ValueError("the slab solver needs at least 2 multigrid levels")
     if nz % (1 << (levels - 1)):
         raise ValueError(f"nz={nz} does not support {levels} levels")
-    for d in range(levels - 2, -1, -1):
+    top = levels - 2 if max_dist_level is None else min(levels - 2, int(max_dist_level))
+    for d in range(top, -1, -1):
         t = nz >> d
         if t % nranks == 0:
             per = (t // nranks) << d
@@ -107,7 +110,7 @@ def _ptr_array(tensors: Sequence[torch.Tensor]):
 
 
 class SlabSolver:
-    """Slab-decomposed operator + homogenized MGPCG for one problem.
+    """Slab-decomposed operator + MGPCG (homogenized or Galerkin V-cycle) for one problem.
 
     grid / fixed_mask are the global problem (every rank passes the same).
     Vectors are lists of per-local-slab device tensors in the vt node layout
@@ -115,11 +118,22 @@ class SlabSolver:
 
     def __init__(self, grid: StructuredGrid, fixed_mask, levels: Optional[int] = None, omega: float = 0.4,
                  nranks: int = 1, rank: int = 0, nlocal: Optional[int] = None, nccl_id: Optional[bytes] = None,
-                 nu: float = 0.3, device: Optional[int] = None, peer: bool = False):
+                 nu: float = 0.3, device: Optional[int] = None, peer: bool = False, scheme: str = "homogenized"):
         require_cuda()
+        if scheme not in ("homogenized", "galerkin"):
+            raise ValueError(f"unknown scheme {scheme!r}")
         self.grid = grid
+        self.scheme = scheme
         self.levels = int(levels) if levels is not None else max_feasible_levels(grid.nelx, grid.nely, grid.nelz)
-        self.plan = plan_slabs(grid.nelz, self.levels, nranks)
+        if scheme == "galerkin":
+            if self.levels < 3:
+                raise ValueError("the Galerkin slab scheme needs at least 3 multigrid levels")
+            self.plan = plan_slabs(grid.nelz, self.levels, nranks, max_dist_level=1)
+            if self.plan.dist_level != 1:
+                raise ValueError(f"the Galerkin slab scheme needs an even number of element layers per slab "
+                                 f"(nz={grid.nelz}, {nranks} slabs)")
+        else:
+            self.plan = plan_slabs(grid.nelz, self.levels, nranks)
         self.nranks, self.rank = nranks, rank
         self.nlocal = nranks if nlocal is None else int(nlocal)
         self.device = torch.cuda.current_device() if device is None else int(device)
@@ -145,6 +159,8 @@ class SlabSolver:
                                      nm.ctypes.data_as(C.c_void_p), self.levels, omega, nranks, rank,
                                      self.nlocal, kb, self.plan.dist_level, idbuf, self.device),
                   "vt_dist_create")
+        if scheme == "galerkin":
+            check(lib.vt_dist_set_scheme(self._h, 1), "vt_dist_set_scheme")
         self.slab_grids = []
         for i in range(self.nlocal):
             g = lib.vt_dist_grid(self._h, i, 0)
@@ -159,7 +175,7 @@ class SlabSolver:
 
     @classmethod
     def from_process_group(cls, grid: StructuredGrid, fixed_mask, levels=None, omega=0.4, group=None,
-                           transport: str = "peer", nu: float = 0.3):
+                           transport: str = "peer", nu: float = 0.3, scheme: str = "homogenized"):
         """One slab per rank of the initialised torch.distributed group.
         transport="peer": IPC handles of every rank's staging block are
         all-gathered over the group; "nccl": the library's NCCL communicator is
@@ -168,7 +184,8 @@ class SlabSolver:
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         if transport == "peer":
-            S = cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nu=nu, peer=True)
+            S = cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nu=nu, peer=True,
+                    scheme=scheme)
             S.connect_peers(group)
             return S
         if transport != "nccl":
@@ -180,7 +197,8 @@ class SlabSolver:
             check(lib.vt_nccl_unique_id(buf, nbytes), "vt_nccl_unique_id")
             obj[0] = bytes(buf)
         dist.broadcast_object_list(obj, src=0, group=group)
-        return cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nccl_id=obj[0], nu=nu)
+        return cls(grid, fixed_mask, levels, omega, nranks=world, rank=rank, nlocal=1, nccl_id=obj[0], nu=nu,
+                   scheme=scheme)
 
     def connect_peers(self, group=None):
         """All-gather the ranks' IPC handles over `group` and map the peers'
@@ -295,7 +313,8 @@ class SlabRun:
 
     def __init__(self, problem, opt, solver: SolverConfig, max_levels=None, omega: float = 0.4,
                  nranks: int = 1, rank: int = 0, nlocal: Optional[int] = None, nccl_id: Optional[bytes] = None,
-                 init_densities=None, group=None, init_displacement=None, peer: bool = False):
+                 init_densities=None, group=None, init_displacement=None, peer: bool = False,
+                 scheme: str = "homogenized"):
         from .design import filter_weights, initial_densities
 
         if solver.preconditioner != "multigrid":
@@ -304,7 +323,7 @@ class SlabRun:
         self.problem, self.opt, self.solver, self.group = problem, opt, solver, group
         fm = problem.boundary.fixed_mask(grid)
         self.S = S = SlabSolver(grid, fm, max_levels, omega, nranks=nranks, rank=rank, nlocal=nlocal,
-                                nccl_id=nccl_id, nu=problem.nu, peer=peer)
+                                nccl_id=nccl_id, nu=problem.nu, peer=peer, scheme=scheme)
         if peer:
             S.connect_peers(group)
         f_ext = problem.boundary.external_force(grid)
@@ -339,13 +358,15 @@ class SlabRun:
 
     @classmethod
     def from_process_group(cls, problem, opt, solver, max_levels=None, omega=0.4, init_densities=None,
-                           group=None, init_displacement=None, transport: str = "peer"):
+                           group=None, init_displacement=None, transport: str = "peer",
+                           scheme: str = "homogenized"):
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         if transport == "peer":
             return cls(problem, opt, solver, max_levels, omega, nranks=world, rank=rank, nlocal=1,
-                       init_densities=init_densities, group=group, init_displacement=init_displacement, peer=True)
+                       init_densities=init_densities, group=group, init_displacement=init_displacement, peer=True,
+                       scheme=scheme)
         if transport != "nccl":
             raise ValueError(f"unknown transport {transport!r}")
         obj = [None]
@@ -357,7 +378,7 @@ class SlabRun:
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls(problem, opt, solver, max_levels, omega, nranks=world, rank=rank, nlocal=1,
                    nccl_id=obj[0], init_densities=init_densities, group=group,
-                   init_displacement=init_displacement)
+                   init_displacement=init_displacement, scheme=scheme)
 
     def solve(self, model) -> SolveReport:
         S = self.S
@@ -430,10 +451,11 @@ class SlabRun:
 
 def run_slabs(problem, opt, solver: SolverConfig = SolverConfig(), max_levels=None, omega: float = 0.4,
               nranks: int = 1, group=None, init_densities=None, start_iteration: int = 0, on_iteration=None,
-              init_displacement=None, transport: str = "peer"):
-    """run() (optimize.py:323-455, homogenized scheme) on z-slabs: all `nranks`
-    slabs in this process, or -- with `group` -- one slab per rank of the group
-    over the `transport` ("peer" or "nccl")."""
+              init_displacement=None, transport: str = "peer", scheme: str = "homogenized"):
+    """run() (optimize.py:323-455) on z-slabs: all `nranks` slabs in this
+    process, or -- with `group` -- one slab per rank of the group over the
+    `transport` ("peer" or "nccl"); scheme "homogenized" or "galerkin" (the
+    reference default, optimize.py:348)."""
     from dataclasses import replace
 
     from .design import DensityField, OptResult, RunRecord, VOLUME_TOL
@@ -441,10 +463,10 @@ def run_slabs(problem, opt, solver: SolverConfig = SolverConfig(), max_levels=No
 
     if group is not None:
         R = SlabRun.from_process_group(problem, opt, solver, max_levels, omega, init_densities, group,
-                                       init_displacement=init_displacement, transport=transport)
+                                       init_displacement=init_displacement, transport=transport, scheme=scheme)
     else:
         R = SlabRun(problem, opt, solver, max_levels, omega, nranks=nranks, init_densities=init_densities,
-                    init_displacement=init_displacement)
+                    init_displacement=init_displacement, scheme=scheme)
     records: List = []
     converged = False
     iteration = start_iteration

@@ -179,3 +179,60 @@ def test_slab_design_loop_with_self_weight():
     for a, b in zip(got.records, ref.records):
         assert abs(a.compliance - b.compliance) <= 1e-9 * abs(b.compliance), (a, b)
     assert np.abs(got.densities.values - ref.densities.values).max() <= 1e-8
+
+
+# ---------------------------------------------------------------- Galerkin (the reference default) on slabs
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_galerkin_slab_vcycle_matches_single(nranks):
+    """Galerkin V-cycle on slabs (levels 0/1 distributed, level 1 matrix-free,
+    stored-matrix tail replicated) against the single-GPU Galerkin V-cycle."""
+    case, grid, rho, rng = _setup(32, 16, 16, seed=4)
+    st = vb.OperatorState(grid, rho, vb.MaterialModel(), case.fixed_mask)
+    H = vb.build_hierarchy(grid, st, 4, scheme="galerkin")
+    S = SlabSolver(grid, case.fixed_mask, levels=4, nranks=nranks, scheme="galerkin")
+    assert S.plan.dist_level == 1
+    S.set_density(rho)
+    r = rng.standard_normal(grid.n_dofs)
+    r[case.fixed_mask] = 0.0
+    ref = H.v_cycle(r)
+    got = S.download(S.v_cycle(S.upload(r)))
+    assert np.abs(got - ref).max() <= 1e-14 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_galerkin_slab_mgcg_matches_single(nranks):
+    case, grid, rho, rng = _setup(32, 16, 32, seed=5)
+    st = vb.OperatorState(grid, rho, vb.MaterialModel(), case.fixed_mask)
+    H = vb.build_hierarchy(grid, st, 4, scheme="galerkin")
+    f = case.f_ext.copy()
+    f[case.fixed_mask] = 0.0
+    cfg = vb.SolverConfig(tolerance=1e-8, max_iterations=300)
+    x_ref, rep_ref = vb.mgcg_solve(st, H, f, cfg=cfg)
+    S = SlabSolver(grid, case.fixed_mask, levels=4, nranks=nranks, scheme="galerkin")
+    S.set_density(rho)
+    x, rep = S.mgcg_solve(S.upload(f), cfg=cfg)
+    assert rep.converged and rep.iterations == rep_ref.iterations, (rep, rep_ref)
+    assert np.abs(S.download(x) - x_ref).max() <= 1e-10 * np.abs(x_ref).max()
+
+
+def test_galerkin_slab_design_loop_matches_single():
+    """run_slabs(scheme="galerkin") against run() with the reference's default
+    scheme, tight solves: same trajectory to rounding."""
+    from paper_2201_12931_b200 import cases
+    from paper_2201_12931_b200.slabs import run_slabs
+
+    prob = cases.cantilever(32, 16, 16)
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * prob.grid.h, max_iterations=5, ch_tol=1e-12)
+    cfg = vb.SolverConfig(tolerance=1e-10, max_iterations=1000)
+    ref = vb.run(prob, opt, cfg, scheme="galerkin", max_levels=4)
+    got = run_slabs(prob, opt, cfg, max_levels=4, nranks=2, scheme="galerkin")
+    for a, b in zip(got.records, ref.records):
+        assert abs(a.compliance - b.compliance) <= 1e-9 * abs(b.compliance), (a, b)
+        assert a.aux_scalars == b.aux_scalars
+    assert np.abs(got.densities.values - ref.densities.values).max() <= 1e-8
+
+
+def test_galerkin_slab_plan_needs_even_layers():
+    case, grid, rho, rng = _setup(16, 8, 8)
+    with pytest.raises(ValueError, match="even number"):
+        SlabSolver(grid, case.fixed_mask, levels=3, nranks=8, scheme="galerkin")

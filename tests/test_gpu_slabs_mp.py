@@ -42,7 +42,7 @@ def _summary(res):
             res.densities.values.copy(), np.asarray(res.displacement).copy())
 
 
-def _worker(rank, world, port, dims, gravity, iters, q):
+def _worker(rank, world, port, dims, gravity, iters, q, scheme="homogenized"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     os.environ.setdefault("VT_PEER_TIMEOUT_S", "120")
     import torch.distributed as dist
@@ -58,11 +58,12 @@ def _worker(rank, world, port, dims, gravity, iters, q):
         opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * prob.grid.h, max_iterations=iters, ch_tol=1e-12)
         cfg = vb.SolverConfig(tolerance=1e-8, max_iterations=300)
         l0 = vb.launch_count()
-        mp_res = _summary(run_slabs(prob, opt, cfg, max_levels=3, group=dist.group.WORLD, transport="peer"))
+        mp_res = _summary(run_slabs(prob, opt, cfg, max_levels=3, group=dist.group.WORLD, transport="peer",
+                                    scheme=scheme))
         launches = vb.launch_count() - l0
         dist.barrier()
         if rank == 0:
-            ref = _summary(run_slabs(prob, opt, cfg, max_levels=3, nranks=world))
+            ref = _summary(run_slabs(prob, opt, cfg, max_levels=3, nranks=world, scheme=scheme))
             q.put(("ok", mp_res, ref, launches))
         else:
             q.put(("ok", None, None, launches))
@@ -72,13 +73,14 @@ def _worker(rank, world, port, dims, gravity, iters, q):
         dist.destroy_process_group()
 
 
-def _run(dims, gravity=None, iters=3, world=2):
+def _run(dims, gravity=None, iters=3, world=2, scheme="homogenized"):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, gravity, iters, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, gravity, iters, q, scheme))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=900) for _ in range(world)]
@@ -101,6 +103,14 @@ def test_two_process_run_bit_identical_to_in_process_slabs(dims):
 
 def test_two_process_run_with_self_weight():
     _, (recs, rho, u), (rrecs, rrho, ru), _ = _run((16, 8, 16), gravity=(2, 1.0, 1e-3), iters=2)
+    assert recs == rrecs
+    assert np.array_equal(rho, rrho)
+    assert np.array_equal(u, ru)
+
+
+def test_two_process_galerkin_run_bit_identical_to_in_process_slabs():
+    """The reference's default scheme with one slab per process."""
+    _, (recs, rho, u), (rrecs, rrho, ru), _ = _run((16, 8, 16), scheme="galerkin", iters=2)
     assert recs == rrecs
     assert np.array_equal(rho, rrho)
     assert np.array_equal(u, ru)
