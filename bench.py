@@ -52,6 +52,8 @@ def _args():
     ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 single-GPU section")
     ap.add_argument("--slabs", action="store_true",
                     help="use the z-slab path even at N=1 (under torchrun; smoke test of the transport)")
+    ap.add_argument("--scheme", default="homogenized", choices=["homogenized", "galerkin"],
+                    help="coarse scheme of the slab solve figure (N > 1)")
     ap.add_argument("--transport", default=os.environ.get("VT_TRANSPORT", "peer"), choices=["peer", "nccl"],
                     help="slab exchange: peer = one kernel per exchange over CUDA IPC / NVLink, nccl = NCCL")
     return ap.parse_args()
@@ -335,7 +337,7 @@ def run_ours(a):
 
         opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
         R = SlabRun.from_process_group(problem, opt, vb.SolverConfig(tolerance=1e-5), spec["levels"], 0.4,
-                                       transport=a.transport)
+                                       transport=a.transport, scheme=a.scheme)
         times, its = [], []
         for it in range(a.simp_iters):
             barrier()
@@ -346,7 +348,7 @@ def run_ours(a):
             times.append(max_over_ranks(time.perf_counter() - ts))
             its.append(rep.iterations)
         solve = _run_summary(times, its)
-        solve.update({"levels": R.S.levels, "dist_level": R.S.plan.dist_level,
+        solve.update({"levels": R.S.levels, "dist_level": R.S.plan.dist_level, "scheme": a.scheme,
                       "note": "SIMP iterations 1..%d on z-slabs (refresh + slab MGPCG, V(1,1), tol 1e-5, "
                               "warm start, then the distributed design step), max over ranks" % a.simp_iters})
         R.S.close()
