@@ -320,6 +320,10 @@ vt_status vt_dist_sensitivities(vt_dist *D, double *const *u, const double *cons
 vt_status vt_dist_gravity_load(vt_dist *D, const double *const *rho, int grav_axis, double grav_coef,
                                const double *const *f_ext, int zero_fixed, double *const *f,
                                void *stream);
+vt_status vt_dist_sensitivities_two_material(vt_dist *D, double *const *u, const double *const *rho,
+                                             const double *const *phi, double p, double kmin, double E,
+                                             double e_ratio, int grav_axis, double grav_coef,
+                                             double *const *dc_rho, double *const *dc_phi, void *stream);
 vt_status vt_dist_filter_create(vt_dist *D, int R, const double *kernel_host);
 vt_status vt_dist_filter_apply(vt_dist *D, const double *const *dc, const double *const *rho,
                                double gamma, double *const *dcf, void *stream);

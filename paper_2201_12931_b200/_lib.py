@@ -113,6 +113,7 @@ _SIGS = {
     "vt_dist_vcycle": (I, [P, P, P, P]),
     "vt_dist_pcg": (I, [P, P, P, I, D, I, C.POINTER(SolveReportC), P]),
     "vt_dist_sensitivities": (I, [P, P, P, D, D, D, I, D, P, P]),
+    "vt_dist_sensitivities_two_material": (I, [P, P, P, P, D, D, D, D, I, D, P, P, P]),
     "vt_dist_gravity_load": (I, [P, P, I, D, P, I, P, P]),
     "vt_dist_filter_create": (I, [P, I, P]),
     "vt_dist_filter_apply": (I, [P, P, P, D, P, P]),

@@ -249,6 +249,21 @@ vt_status vt_dist_sensitivities(vt_dist* D, double* const* u, const double* cons
   return VT_OK;
 }
 
+// (dc_rho, dc_phi) of the two-material law on every local slab (u's ghost
+// planes refreshed first) [extends optimize.py:195-213; DESIGN.md 3.5]
+vt_status vt_dist_sensitivities_two_material(vt_dist* D, double* const* u, const double* const* rho,
+                                             const double* const* phi, double p, double kmin, double E,
+                                             double e_ratio, int grav_axis, double grav_coef,
+                                             double* const* dc_rho, double* const* dc_phi, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<double*> uu(u, u + D->nlocal);
+  VT_TRY(halo_nodes(D, 0, uu, s));
+  for (int i = 0; i < D->nlocal; ++i)
+    VT_TRY(vt_sensitivities_two_material(D->sl[i].lv[0], u[i], rho[i], phi[i], p, kmin, E, e_ratio,
+                                         grav_axis, grav_coef, dc_rho[i], dc_phi[i], stream));
+  return VT_OK;
+}
+
 // f = gravity load of rho (+ f_ext), zero on fixed dofs when zero_fixed
 vt_status vt_dist_gravity_load(vt_dist* D, const double* const* rho, int grav_axis, double grav_coef,
                                const double* const* f_ext, int zero_fixed, double* const* f,

@@ -42,7 +42,7 @@ from .material import gravity_coefficient
 from .stiffness_op import OperatorState, as_device
 
 __all__ = ["TwoMaterialRecord", "TwoMaterialResult", "initial_phases", "sensitivities_two_material",
-           "run_two_material"]
+           "run_two_material", "run_two_material_slabs"]
 
 
 @dataclass
@@ -188,3 +188,128 @@ def run_two_material(problem: Problem, opt: OptConfig, phase_frac: float, e_rati
             converged = True
             break
     return TwoMaterialResult(R.densities(), R.phases(), R.displacement(), records, converged, iteration)
+
+
+# ---------------------------------------------------------------- on z-slabs
+def _slab_run_class():
+    from .slabs import SlabRun, _ptr_array
+
+    class SlabTwoMaterialRun(SlabRun):
+        """SlabRun with the second design field: per-slab two-material scale
+        (+ the density the homogenized coarse levels average), the distributed
+        two-material sensitivities (u halo), and the distributed filter / OC /
+        change for both fields -- TwoMaterialRun's steps on slabs."""
+
+        def __init__(self, problem, opt, phase_frac, e_ratio, solver, max_levels=None, omega=0.4, nranks=1,
+                     group=None, scheme="homogenized", **kw):
+            _check_ratio(e_ratio)
+            if not 0 < phase_frac <= 1:
+                raise ValueError("phase_frac must lie in (0, 1]")
+            super().__init__(problem, opt, solver, max_levels, omega, nranks=nranks, group=group, scheme=scheme,
+                             **kw)
+            self.e_ratio, self.phase_frac = float(e_ratio), float(phase_frac)
+            phi0 = torch.as_tensor(initial_phases(problem.regions, phase_frac).values, device=self.rho[0].device)
+            nxy = problem.grid.nelx * problem.grid.nely
+            self.phi = [phi0[dg.k0 * nxy:dg.k1 * nxy].clone() for dg in self.S.slab_grids]
+            self.phi_new = [torch.empty_like(p) for p in self.phi]
+            self.rho_h = [torch.empty_like(r) for r in self.rho]
+            self.dcp = [torch.empty_like(r) for r in self.rho]
+            self.dcpf = [torch.empty_like(r) for r in self.rho]
+
+        def solve(self, model):
+            S = self.S
+            S.model = model
+            for dg, r, ph, sc, rh in zip(S.slab_grids, self.rho, self.phi, S.scales, self.rho_h):
+                check(lib.vt_scale_two_material(dg.handle, ptr(r), ptr(ph), model.p, model.kmin_frac, model.E,
+                                                self.e_ratio, ptr(sc), ptr(rh), stream_ptr()))
+            check(lib.vt_dist_refresh(S._h, _ptr_array(self.rho_h), _ptr_array(S.scales), model.p,
+                                      model.kmin_frac, model.E, stream_ptr()), "vt_dist_refresh")
+            if self.gravity is not None:
+                check(lib.vt_dist_gravity_load(S._h, _ptr_array(self.rho), int(self.gravity.axis), self._gco(),
+                                               _ptr_array(self.f_ext), 1, _ptr_array(self.f), stream_ptr()))
+            self.u, rep = S.mgcg_solve(self.f, u_prev=self.u, cfg=self.solver)
+            return rep
+
+        def _oc(self, x, dcf, opt, out):
+            lam, steps = C.c_double(), C.c_int()
+            check(lib.vt_dist_oc_update(self.S._h, _ptr_array(x), _ptr_array(self.cls), _ptr_array(dcf),
+                                        _ptr_array(self.dv), float(opt.volfrac), float(opt.move), float(opt.eta),
+                                        float(opt.q), _ptr_array(out), C.byref(lam), C.byref(steps),
+                                        stream_ptr()))
+
+        def _change(self, a, b, want_change=True, want_mean=True):
+            ch, vol = C.c_double(), C.c_double()
+            check(lib.vt_dist_change_volume(self.S._h, _ptr_array(a), _ptr_array(b), _ptr_array(self.cls),
+                                            C.byref(ch) if want_change else None,
+                                            C.byref(vol) if want_mean else None, stream_ptr()))
+            return ch.value, vol.value
+
+        def design_step(self, model):
+            """(c, change, volume, phase_volume), TwoMaterialRun.design_step on slabs."""
+            S, opt = self.S, self.opt
+            c = S.dot(self.f, self.u)
+            gax, gco = (int(self.gravity.axis), self._gco()) if self.gravity is not None else (-1, 0.0)
+            check(lib.vt_dist_sensitivities_two_material(S._h, _ptr_array(self.u), _ptr_array(self.rho),
+                                                         _ptr_array(self.phi), model.p, model.kmin_frac, model.E,
+                                                         self.e_ratio, gax, gco, _ptr_array(self.dc),
+                                                         _ptr_array(self.dcp), stream_ptr()))
+            check(lib.vt_dist_filter_apply(S._h, _ptr_array(self.dc), _ptr_array(self.rho), float(opt.gamma),
+                                           _ptr_array(self.dcf), stream_ptr()))
+            self._oc(self.rho, self.dcf, opt, self.rho_new)
+            change, vol = self._change(self.rho_new, self.rho)
+            if self.e_ratio != 1.0:  # at e_ratio = 1 phi has no influence (dc_phi = 0)
+                check(lib.vt_dist_filter_apply(S._h, _ptr_array(self.dcp), _ptr_array(self.phi), float(opt.gamma),
+                                               _ptr_array(self.dcpf), stream_ptr()))
+                self._oc(self.phi, self.dcpf, replace(opt, volfrac=self.phase_frac), self.phi_new)
+                chp, _ = self._change(self.phi_new, self.phi, want_mean=False)
+                change = max(change, chp)
+                self.phi, self.phi_new = self.phi_new, self.phi
+            _, pv = self._change(self.phi, self.phi, want_change=False)
+            self.rho, self.rho_new = self.rho_new, self.rho
+            return c, change, vol, pv
+
+        def phases(self) -> np.ndarray:
+            return self._gather(self.phi).cpu().numpy()
+
+    return SlabTwoMaterialRun
+
+
+def run_two_material_slabs(problem: Problem, opt: OptConfig, phase_frac: float, e_ratio: float = 0.5,
+                           solver: SolverConfig = SolverConfig(), scheme: str = "homogenized",
+                           max_levels: Optional[int] = None, omega: float = 0.4, nranks: int = 1,
+                           group=None, transport: str = "peer") -> TwoMaterialResult:
+    """run_two_material on z-slabs: all `nranks` slabs in this process, or one
+    slab per rank of `group` (peer / nccl transport), either coarse scheme."""
+    Cls = _slab_run_class()
+    if group is not None:
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if transport != "peer":
+            raise ValueError("run_two_material_slabs with a process group uses the peer transport")
+        R = Cls(problem, opt, phase_frac, e_ratio, solver, max_levels, omega, nranks=world, group=group,
+                scheme=scheme, rank=rank, nlocal=1, peer=True)
+    else:
+        R = Cls(problem, opt, phase_frac, e_ratio, solver, max_levels, omega, nranks=nranks, scheme=scheme)
+    records: List[TwoMaterialRecord] = []
+    converged = False
+    iteration = 0
+    try:
+        while iteration < opt.max_iterations:
+            t0 = time.perf_counter()
+            model_k = replace(problem.model, p=opt.penal_at(iteration))
+            rep = R.solve(model_k)
+            c, ch, vol, pvol = R.design_step(model_k)
+            iteration += 1
+            if abs(vol - opt.volfrac) > VOLUME_TOL:
+                raise NumericalError(f"volume constraint violated after update: {vol} vs {opt.volfrac}")
+            records.append(TwoMaterialRecord(iteration, c, vol, ch, rep.iterations, rep.final_rel_residual,
+                                             time.perf_counter() - t0, rep.aux_vector_scalars, pvol))
+            if ch <= opt.ch_tol:
+                converged = True
+                break
+        return TwoMaterialResult(DensityField(R.densities(), problem.regions),
+                                 DensityField(R.phases(), problem.regions), R.displacement(), records, converged,
+                                 iteration)
+    finally:
+        R.S.close()

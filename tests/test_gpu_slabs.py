@@ -236,3 +236,23 @@ def test_galerkin_slab_plan_needs_even_layers():
     case, grid, rho, rng = _setup(16, 8, 8)
     with pytest.raises(ValueError, match="even number"):
         SlabSolver(grid, case.fixed_mask, levels=3, nranks=8, scheme="galerkin")
+
+
+@pytest.mark.parametrize("scheme", ["homogenized", "galerkin"])
+def test_two_material_slabs_match_single(scheme):
+    """Two-material SIMP (BASELINE cfg4's extension) on 2 slabs against the
+    single-GPU run_two_material, tight solves."""
+    from paper_2201_12931_b200 import cases
+    from paper_2201_12931_b200.multimaterial import run_two_material, run_two_material_slabs
+
+    prob = cases.cantilever(32, 16, 16)
+    opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * prob.grid.h, max_iterations=4, ch_tol=1e-12)
+    cfg = vb.SolverConfig(tolerance=1e-10, max_iterations=1000)
+    ref = run_two_material(prob, opt, phase_frac=0.5, e_ratio=0.5, solver=cfg, scheme=scheme, max_levels=4)
+    got = run_two_material_slabs(prob, opt, phase_frac=0.5, e_ratio=0.5, solver=cfg, scheme=scheme,
+                                 max_levels=4, nranks=2)
+    for a, b in zip(got.records, ref.records):
+        assert abs(a.compliance - b.compliance) <= 1e-9 * abs(b.compliance), (a, b)
+        assert abs(a.phase_volume - b.phase_volume) <= 1e-9
+    assert np.abs(got.densities.values - ref.densities.values).max() <= 1e-8
+    assert np.abs(got.phases.values - ref.phases.values).max() <= 1e-8
