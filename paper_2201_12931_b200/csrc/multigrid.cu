@@ -14,6 +14,8 @@
 
 #include <atomic>
 
+#include <stdlib.h>
+
 #include "vt_internal.h"
 #include "vt_pcg.cuh"
 
@@ -247,6 +249,132 @@ __global__ void __launch_bounds__(MG_THREADS)
   }
 }
 
+// ---- TMA-streamed restriction (large levels).  Same units and the same
+// arithmetic as restrict_kernel (bit-identical), but each unit's three fine
+// planes x (2 XR_RJ + 1) rows x (2 XR_RI + 1) nodes arrive by three TMA loads
+// into a ring of XR_NS stages, issued XR_NS units ahead by one thread: the
+// row walk of restrict_kernel waits on its own loads unit by unit (ncu:
+// long-scoreboard + barrier stalls, ~3 TB/s); here the loads of the next
+// units are in flight while this unit's z / y / x passes run.
+#ifndef VT_XR_NS
+#define VT_XR_NS 2
+#endif
+constexpr int XR_RI = 33, XR_RJ = 4, XR_NS = VT_XR_NS;
+constexpr int XR_W = 3 * (2 * XR_RI + 1);      // fine dofs of a staged row (201)
+constexpr int XR_BW = XR_W + 1;                // TMA box width (even start one dof early)
+constexpr int XR_BR = 2 * XR_RJ + 1;           // staged fine rows
+constexpr int XR_PLANE_B = ((XR_BW * XR_BR * 8 + 127) / 128) * 128;
+constexpr int XR_STAGE_B = 3 * XR_PLANE_B;
+constexpr int XR_SMEM = XR_NS * XR_STAGE_B + XR_BR * XR_W * 8 + XR_NS * 8 + 128;
+
+struct XrUnits {
+  int kb, ke, nJb, nIb;
+};
+
+__device__ __forceinline__ void xr_issue(const CUtensorMap* m, const Geom& gf, const XrUnits& U, long long unit,
+                                         unsigned char* stage, uint64_t* bar) {
+  const int ib = (int)(unit % U.nIb);
+  const long long r0 = unit / U.nIb;
+  const int jb = (int)(r0 % U.nJb);
+  const int K = (int)(r0 / U.nJb) + U.kb;
+  const int x0 = 3 * (2 * ib * XR_RI - 1) - 1;  // one dof early: even (16-byte) start
+  const int y0 = 2 * jb * XR_RJ - 1;
+  const int p0 = 2 * K - gf.k0 + 1;
+  mbar_expect_tx(bar, 3 * XR_BW * XR_BR * 8);
+  tma_load_3d(stage, m, bar, x0, y0, p0);                        // plane 2K
+  tma_load_3d(stage + XR_PLANE_B, m, bar, x0, y0, p0 + 1);       // plane 2K + 1
+  tma_load_3d(stage + 2 * XR_PLANE_B, m, bar, x0, y0, p0 - 1);   // plane 2K - 1
+}
+
+__global__ void __launch_bounds__(MG_THREADS)
+    restrict_tma_kernel(const __grid_constant__ CUtensorMap mf, Geom gf, Geom gc, const uint8_t* __restrict__ mc,
+                        double* __restrict__ fc, const int* stop, XrUnits U) {
+  griddep_wait();
+  if (stop && *(volatile const int*)stop) return;
+  extern __shared__ __align__(128) unsigned char xsm[];
+  double* tzs = reinterpret_cast<double*>(xsm + XR_NS * XR_STAGE_B);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tzs + XR_BR * XR_W);
+  const long long units = (long long)(U.ke - U.kb) * U.nJb * U.nIb;
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&mf);
+    for (int i = 0; i < XR_NS; ++i) mbar_init(&bars[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < XR_NS; ++i) {
+      const long long u = blockIdx.x + (long long)i * gridDim.x;
+      if (u < units) xr_issue(&mf, gf, U, u, xsm + i * XR_STAGE_B, &bars[i]);
+    }
+  int it = 0;
+  for (long long unit = blockIdx.x; unit < units; unit += gridDim.x, ++it) {
+    const int slot = it % XR_NS;
+    const int ib = (int)(unit % U.nIb);
+    const long long r0 = unit / U.nIb;
+    const int jb = (int)(r0 % U.nJb);
+    const int K = (int)(r0 / U.nJb) + U.kb;
+    const int J0 = jb * XR_RJ, I0 = ib * XR_RI;
+    const int nJ = min(XR_RJ, gc.ny + 1 - J0), nI = min(XR_RI, gc.nx + 1 - I0);
+    const bool ok1 = 2 * K + 1 <= gf.nz, ok2 = K >= 1;
+    mbar_wait(&bars[slot], (uint32_t)((it / XR_NS) & 1));
+    const double* st = reinterpret_cast<const double*>(xsm + slot * XR_STAGE_B);
+    const double* s1 = st + XR_PLANE_B / 8;
+    const double* s2 = st + 2 * XR_PLANE_B / 8;
+    // phase 1: z pass of the staged rows (out-of-grid rows / dofs arrive as 0 and are never read)
+    for (int e = threadIdx.x; e < XR_BR * XR_W; e += blockDim.x) {
+      const int r = e / XR_W, c = e - r * XR_W;
+      const int o = r * XR_BW + c + 1;
+      double v = st[o];
+      if (ok1) v = __dadd_rn(v, 0.5 * s1[o]);
+      if (ok2) v = __dadd_rn(v, 0.5 * s2[o]);
+      tzs[e] = v;
+    }
+    __syncthreads();
+    // the stage is free: refill it XR_NS units ahead
+    if (threadIdx.x == 0) {
+      const long long nu = unit + (long long)XR_NS * gridDim.x;
+      if (nu < units) xr_issue(&mf, gf, U, nu, xsm + slot * XR_STAGE_B, &bars[slot]);
+    }
+    // phase 2: y pass then x pass per coarse dof (restrict_kernel's phase 2)
+    const int p = K - gc.k0 + 1;
+    const int cw = 3 * nI;
+    for (int e = threadIdx.x; e < cw; e += blockDim.x) {
+      const int ii = e / 3, c = e - 3 * ii;
+      const int I = I0 + ii;
+      const bool oki1 = 2 * I + 1 <= gf.nx, oki2 = I >= 1;
+      double* out = fc + node_off(gc, p, J0, I) * 3 + c;
+      const uint8_t* mrow = mc + mask_off(gc, p, J0, I);
+#pragma unroll 2
+      for (int jj = 0; jj < nJ; ++jj) {
+        const int J = J0 + jj;
+        const bool okj1 = 2 * J + 1 <= gf.ny, okj2 = J >= 1;
+        const double* rw = tzs + (2 * jj + 1) * XR_W + 3 * (2 * ii + 1) + c;
+        double ty[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const int dx = b == 0 ? 0 : (b == 1 ? 3 : -3);
+          if ((b == 1 && !oki1) || (b == 2 && !oki2)) {
+            ty[b] = 0.0;
+            continue;
+          }
+          double v = rw[dx];
+          if (okj1) v = __dadd_rn(v, 0.5 * rw[XR_W + dx]);
+          if (okj2) v = __dadd_rn(v, 0.5 * rw[-XR_W + dx]);
+          ty[b] = v;
+        }
+        double v = ty[0];
+        if (oki1) v = __dadd_rn(v, 0.5 * ty[1]);
+        if (oki2) v = __dadd_rn(v, 0.5 * ty[2]);
+        const unsigned m = mrow[(long long)jj * gc.mp];
+        out[(long long)jj * gc.rp * 3] = ((m >> c) & 1u) ? 0.0 : v;
+      }
+    }
+    __syncthreads();  // tzs is rewritten by the next unit
+  }
+}
+
+static bool g_xr_tma = true;  // VT_XR_TMA=0: always the row-walk kernel (A/B)
+
 // kb < 0: every coarse plane the coarse grid owns
 vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, const int* stop,
                           int kb, int ke, cudaStream_t s) {
@@ -255,6 +383,32 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
     ke = C->g.k1 + C->g.last;
   }
   if (ke <= kb) return VT_OK;
+  // large fine levels: the TMA-streamed kernel (one CTA per 8 fine dof rows
+  // of staging is not worth it below ~1M fine dofs)
+  static int xr_env = -1;
+  if (xr_env < 0) {
+    const char* e = getenv("VT_XR_TMA");
+    xr_env = e ? atoi(e) : 1;
+    g_xr_tma = xr_env != 0;
+  }
+  if (g_xr_tma && (long long)F->g.nplane * (F->g.pB - F->g.pA) >= (1LL << 20)) {
+    const CUtensorMap* m = xfer_map(F, rf, XR_BW, XR_BR);
+    if (m) {
+      static bool attr = false;
+      if (!attr) {
+        VT_CUDA(cudaFuncSetAttribute(restrict_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, XR_SMEM));
+        attr = true;
+      }
+      XrUnits U{kb, ke, (C->g.ny + 1 + XR_RJ - 1) / XR_RJ, (C->g.nx + 1 + XR_RI - 1) / XR_RI};
+      const long long units = (long long)(ke - kb) * U.nJb * U.nIb;
+      const CUtensorMap mv = *m;
+      launch_pdl(restrict_tma_kernel, fit_grid(units, 1, C->nsm * (XR_NS >= 3 ? 1 : 2)), MG_THREADS, XR_SMEM, s,
+                 mv, F->g, C->g, (const uint8_t*)C->mask, fc, stop, U);
+      count_launch();
+      VT_CUDA(cudaGetLastError());
+      return VT_OK;
+    }
+  }
   const RestrictBlk blk = restrict_blocks(C->g, kb, ke, C->nsm);
   const size_t sm = restrict_smem(blk);
   static bool attr = false;

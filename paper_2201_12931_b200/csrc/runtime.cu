@@ -130,6 +130,19 @@ const CUtensorMap* vec_map(vt_grid* G, const void* ptr) {
   return &(G->vec_maps[ptr] = m);
 }
 
+// fine-level node vector seen as (dofs of a row, rows, planes) with a
+// (box_x dofs, box_y rows, 1 plane) box: the staged blocks of the restriction
+const CUtensorMap* xfer_map(vt_grid* G, const void* ptr, unsigned box_x, unsigned box_y) {
+  auto it = G->xfer_maps.find(ptr);
+  if (it != G->xfer_maps.end()) return &it->second;
+  CUtensorMap m;
+  const Geom& g = G->g;
+  if (!encode3d(&m, ptr, 3ull * (g.nx + 1), g.ny + 1, g.P, 24ull * g.rp, 24ull * g.rp * (g.ny + 1), box_x, box_y))
+    return nullptr;
+  if (G->xfer_maps.size() > 256) G->xfer_maps.clear();
+  return &(G->xfer_maps[ptr] = m);
+}
+
 const CUtensorMap* elem_map(vt_grid* G, const void* ptr) {
   auto it = G->elem_maps.find(ptr);
   if (it != G->elem_maps.end()) return &it->second;

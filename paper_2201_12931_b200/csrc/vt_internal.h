@@ -100,6 +100,7 @@ struct vt_grid {
   int nsm = 148;
   std::map<const void*, CUtensorMap> vec_maps;   // node-vector TMA descriptors
   std::map<const void*, CUtensorMap> elem_maps;  // element-field TMA descriptors
+  std::map<const void*, CUtensorMap> xfer_maps;  // node-vector descriptors of the TMA restriction
   // PCG workspace (lazily allocated)
   double *w_x = nullptr, *w_f = nullptr, *w_r = nullptr, *w_p = nullptr, *w_q = nullptr,
          *w_z = nullptr, *w_t = nullptr, *w_d = nullptr;
@@ -150,6 +151,7 @@ vt_status hier_refresh_levels(vt_hier* H, double p, double kmin, double E, cudaS
 // TMA descriptors (cached per device pointer)
 const CUtensorMap* vec_map(vt_grid* G, const void* ptr);
 const CUtensorMap* elem_map(vt_grid* G, const void* ptr);
+const CUtensorMap* xfer_map(vt_grid* G, const void* ptr, unsigned box_x, unsigned box_y);
 
 // kernel launchers (hex8_apply.cu)
 Hex8Launch hex8_plan(const Geom& g, int nsm);

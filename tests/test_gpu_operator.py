@@ -89,7 +89,7 @@ def _hier(g, tag):
     return st, vb.build_hierarchy(grid, st, int(g[f"{tag}_levels"]), scheme="homogenized")
 
 
-@pytest.mark.parametrize("dims", [(264, 36, 12), (128, 16, 8), (4, 4, 4)])
+@pytest.mark.parametrize("dims", [(264, 36, 12), (128, 16, 8), (4, 4, 4), (132, 68, 64)])
 def test_transfers_bit_identical_across_blocks(dims):
     """Restriction / prolongation stay bit-identical to the axis passes when the
     coarse level spans several (row block, node block) units of the staged
