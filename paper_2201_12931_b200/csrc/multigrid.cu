@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(MG_THREADS)
 #define VT_XR_NS 2
 #endif
 constexpr int XR_RI = 33, XR_RJ = 4, XR_NS = VT_XR_NS;
+constexpr int XR_IT = (XR_RJ * 3 * XR_RI + MG_THREADS - 1) / MG_THREADS;  // phase-2 items per thread
 constexpr int XR_W = 3 * (2 * XR_RI + 1);      // fine dofs of a staged row (201)
 constexpr int XR_BW = XR_W + 1;                // TMA box width (even start one dof early)
 constexpr int XR_BR = 2 * XR_RJ + 1;           // staged fine rows
@@ -316,6 +317,20 @@ __global__ void __launch_bounds__(MG_THREADS)
     const int J0 = jb * XR_RJ, I0 = ib * XR_RI;
     const int nJ = min(XR_RJ, gc.ny + 1 - J0), nI = min(XR_RI, gc.nx + 1 - I0);
     const bool ok1 = 2 * K + 1 <= gf.nz, ok2 = K >= 1;
+    const int p = K - gc.k0 + 1;
+    const int cw = 3 * nI, nit = nJ * cw;
+    // phase-2 items of this thread (at most XR_IT): their coarse masks are
+    // loaded now, so the global-load latency overlaps the wait and phase 1
+    unsigned mk[XR_IT];
+#pragma unroll
+    for (int q = 0; q < XR_IT; ++q) {
+      const int t = threadIdx.x + q * MG_THREADS;
+      mk[q] = 0;
+      if (t < nit) {
+        const int jj = t / cw, e = t - jj * cw;
+        mk[q] = mc[mask_off(gc, p, J0 + jj, I0 + e / 3)];
+      }
+    }
     mbar_wait(&bars[slot], (uint32_t)((it / XR_NS) & 1));
     const double* st = reinterpret_cast<const double*>(xsm + slot * XR_STAGE_B);
     const double* s1 = st + XR_PLANE_B / 8;
@@ -335,39 +350,35 @@ __global__ void __launch_bounds__(MG_THREADS)
       const long long nu = unit + (long long)XR_NS * gridDim.x;
       if (nu < units) xr_issue(&mf, gf, U, nu, xsm + slot * XR_STAGE_B, &bars[slot]);
     }
-    // phase 2: y pass then x pass per coarse dof (restrict_kernel's phase 2)
-    const int p = K - gc.k0 + 1;
-    const int cw = 3 * nI;
-    for (int e = threadIdx.x; e < cw; e += blockDim.x) {
-      const int ii = e / 3, c = e - 3 * ii;
-      const int I = I0 + ii;
-      const bool oki1 = 2 * I + 1 <= gf.nx, oki2 = I >= 1;
-      double* out = fc + node_off(gc, p, J0, I) * 3 + c;
-      const uint8_t* mrow = mc + mask_off(gc, p, J0, I);
-#pragma unroll 2
-      for (int jj = 0; jj < nJ; ++jj) {
-        const int J = J0 + jj;
-        const bool okj1 = 2 * J + 1 <= gf.ny, okj2 = J >= 1;
-        const double* rw = tzs + (2 * jj + 1) * XR_W + 3 * (2 * ii + 1) + c;
-        double ty[3];
+    // phase 2: y pass then x pass per coarse dof (restrict_kernel's arithmetic),
+    // every (row, dof) of the unit an independent item
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const int dx = b == 0 ? 0 : (b == 1 ? 3 : -3);
-          if ((b == 1 && !oki1) || (b == 2 && !oki2)) {
-            ty[b] = 0.0;
-            continue;
-          }
-          double v = rw[dx];
-          if (okj1) v = __dadd_rn(v, 0.5 * rw[XR_W + dx]);
-          if (okj2) v = __dadd_rn(v, 0.5 * rw[-XR_W + dx]);
-          ty[b] = v;
+    for (int q = 0; q < XR_IT; ++q) {
+      const int t = threadIdx.x + q * MG_THREADS;
+      if (t >= nit) break;
+      const int jj = t / cw, e = t - jj * cw;
+      const int ii = e / 3, c = e - 3 * ii;
+      const int I = I0 + ii, J = J0 + jj;
+      const bool oki1 = 2 * I + 1 <= gf.nx, oki2 = I >= 1;
+      const bool okj1 = 2 * J + 1 <= gf.ny, okj2 = J >= 1;
+      const double* rw = tzs + (2 * jj + 1) * XR_W + 3 * (2 * ii + 1) + c;
+      double ty[3];
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int dx = b == 0 ? 0 : (b == 1 ? 3 : -3);
+        if ((b == 1 && !oki1) || (b == 2 && !oki2)) {
+          ty[b] = 0.0;
+          continue;
         }
-        double v = ty[0];
-        if (oki1) v = __dadd_rn(v, 0.5 * ty[1]);
-        if (oki2) v = __dadd_rn(v, 0.5 * ty[2]);
-        const unsigned m = mrow[(long long)jj * gc.mp];
-        out[(long long)jj * gc.rp * 3] = ((m >> c) & 1u) ? 0.0 : v;
+        double v = rw[dx];
+        if (okj1) v = __dadd_rn(v, 0.5 * rw[XR_W + dx]);
+        if (okj2) v = __dadd_rn(v, 0.5 * rw[-XR_W + dx]);
+        ty[b] = v;
       }
+      double v = ty[0];
+      if (oki1) v = __dadd_rn(v, 0.5 * ty[1]);
+      if (oki2) v = __dadd_rn(v, 0.5 * ty[2]);
+      fc[node_off(gc, p, J, I) * 3 + c] = ((mk[q] >> c) & 1u) ? 0.0 : v;
     }
     __syncthreads();  // tzs is rewritten by the next unit
   }
