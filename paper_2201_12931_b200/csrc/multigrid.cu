@@ -259,7 +259,10 @@ __global__ void __launch_bounds__(MG_THREADS)
 #ifndef VT_XR_NS
 #define VT_XR_NS 2
 #endif
-constexpr int XR_RI = 33, XR_RJ = 4, XR_NS = VT_XR_NS;
+#ifndef VT_XR_RJ
+#define VT_XR_RJ 4
+#endif
+constexpr int XR_RI = 33, XR_RJ = VT_XR_RJ, XR_NS = VT_XR_NS;
 constexpr int XR_IT = (XR_RJ * 3 * XR_RI + MG_THREADS - 1) / MG_THREADS;  // phase-2 items per thread
 constexpr int XR_W = 3 * (2 * XR_RI + 1);      // fine dofs of a staged row (201)
 constexpr int XR_BW = XR_W + 1;                // TMA box width (even start one dof early)
@@ -267,6 +270,7 @@ constexpr int XR_BR = 2 * XR_RJ + 1;           // staged fine rows
 constexpr int XR_PLANE_B = ((XR_BW * XR_BR * 8 + 127) / 128) * 128;
 constexpr int XR_STAGE_B = 3 * XR_PLANE_B;
 constexpr int XR_SMEM = XR_NS * XR_STAGE_B + XR_BR * XR_W * 8 + XR_NS * 8 + 128;
+constexpr int XR_CPS = (220 * 1024) / XR_SMEM < 4 ? (220 * 1024) / XR_SMEM : 4;  // resident CTAs per SM
 
 struct XrUnits {
   int kb, ke, nJb, nIb;
@@ -413,7 +417,7 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
       XrUnits U{kb, ke, (C->g.ny + 1 + XR_RJ - 1) / XR_RJ, (C->g.nx + 1 + XR_RI - 1) / XR_RI};
       const long long units = (long long)(ke - kb) * U.nJb * U.nIb;
       const CUtensorMap mv = *m;
-      launch_pdl(restrict_tma_kernel, fit_grid(units, 1, C->nsm * (XR_NS >= 3 ? 1 : 2)), MG_THREADS, XR_SMEM, s,
+      launch_pdl(restrict_tma_kernel, fit_grid(units, 1, C->nsm * XR_CPS), MG_THREADS, XR_SMEM, s,
                  mv, F->g, C->g, (const uint8_t*)C->mask, fc, stop, U);
       count_launch();
       VT_CUDA(cudaGetLastError());
