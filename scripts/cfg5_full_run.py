@@ -58,6 +58,6 @@ out = {"workload": "cfg5 cantilever 768x384x384, 113246208 elements, 341955075 d
        "total_s": total, "s_per_simp_iter": sum(x["wall_s"] for x in lines) / len(lines),
        "cg_iters_total": sum(x["cg"] for x in lines),
        "compliance_first_last": [lines[0]["c"], lines[-1]["c"]], "change_last": lines[-1]["change"],
-       "hbm_peak_gb": torch.cuda.max_memory_allocated() / 1e9,
+       "device_memory_used_gb": (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9,
        "note": "public run() at the reference defaults (tol 1e-5, CG cap 200, ch_tol 0.01, max 300 iterations)"}
 print(json.dumps(out))
