@@ -1,3 +1,7 @@
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <atomic>
 // libvoxb200 runtime: grids, TMA descriptors, layout conversion, the C ABI
 // of the operator, and the PCG driver [ref: solver.py:62-191].
 //
@@ -278,6 +282,8 @@ vt_status vt_grid_destroy(vt_grid* G) {
   cudaFree(G->mask); cudaFree(G->partial); cudaFree(G->scalars); cudaFreeHost(G->host_scalars);
   cudaFree(G->scratch); cudaFree(G->scratch2);
   cudaFree(G->io_stage); cudaFree(G->io_stage_out); cudaFree(G->io_raw); cudaFree(G->io_proj); cudaFree(G->io_v);
+  if (G->io_pin_in) cudaFreeHost(G->io_pin_in);
+  if (G->io_pin_out) cudaFreeHost(G->io_pin_out);
   if (G->io_in) cudaStreamDestroy(G->io_in);
   if (G->io_out) cudaStreamDestroy(G->io_out);
   for (cudaEvent_t e : G->io_ev)
@@ -344,8 +350,25 @@ vt_status vt_apply_projected(vt_grid* G, const double* scale, const double* u, d
 // H2D copy of chunk c+1 (copy engine 1), the operator on chunk c (SMs) and the
 // D2H copy of chunk c-1 (copy engine 2) overlap, so the call costs about one
 // PCIe transfer instead of two plus the kernel [ref: operator.py:154-165].
-// Host arrays are the reference's flat (n_dofs,) order (pinned memory gives
-// full PCIe bandwidth; pageable works through the driver's staging).  Blocking.
+// Host arrays are the reference's flat (n_dofs,) order.  Page-locked arrays
+// are copied directly; pageable ones (a stock numpy array) go through the
+// grid's page-locked staging buffers, filled / drained chunk by chunk by a few
+// host threads so the host copies overlap the PCIe transfers (the driver's own
+// pageable path serialises a bounce-buffer copy per transfer).  Blocking.
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+static int io_threads() {
+  const unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(8u, hc ? hc : 1u));
+}
+
 vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, double* hv,
                         int nchunks, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
@@ -373,19 +396,57 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
   cudaEvent_t ev_done = G->io_ev[32];
   const double* hsrc = hu + (size_t)g.k0 * dplane;
   double* hdst = hv + (size_t)g.k0 * dplane;
+  const bool stage_in = !host_pinned(hu), stage_out = !host_pinned(hv);
+  if ((stage_in && !G->io_pin_in) || (stage_out && !G->io_pin_out)) {
+    double** bufs[2] = {&G->io_pin_in, &G->io_pin_out};
+    for (double** b : bufs)
+      if (!*b) VT_CUDA(cudaMallocHost(b, (size_t)nown * dplane * sizeof(double)));
+  }
+  const double* src = stage_in ? G->io_pin_in : hsrc;
+  double* dst = stage_out ? G->io_pin_out : hdst;
+  auto chunk = [&](int c, size_t* off, size_t* cnt) {
+    *off = (size_t)(pb[c] - g.pA) * dplane;
+    *cnt = (size_t)(pb[c + 1] - pb[c]) * dplane;
+  };
+  // host staging of the input: the threads copy chunk after chunk, each a
+  // slice of it; the H2D of chunk c is issued once all slices of c are in
+  const int T = (stage_in || stage_out) ? io_threads() : 0;
+  std::vector<std::atomic<int>> in_done(nch);
+  for (auto& a : in_done) a.store(0);
+  std::vector<std::thread> workers;
+  if (stage_in) {
+    for (int t = 0; t < T; ++t)
+      workers.emplace_back([&, t]() {
+        for (int c = 0; c < nch; ++c) {
+          size_t off, cnt;
+          chunk(c, &off, &cnt);
+          const size_t a = off + cnt * t / T, b = off + cnt * (t + 1) / T;
+          memcpy(G->io_pin_in + a, hsrc + a, (b - a) * sizeof(double));
+          in_done[c].fetch_add(1, std::memory_order_release);
+        }
+      });
+  }
   // the copy streams must not run ahead of work already queued on s
   VT_CUDA(cudaEventRecord(ev_done, s));
   VT_CUDA(cudaStreamWaitEvent(G->io_in, ev_done, 0));
   VT_CUDA(cudaStreamWaitEvent(G->io_out, ev_done, 0));
+  vt_status st = VT_OK;
   // the input copy stream carries copies only, so the H2D engine never waits
   // for a kernel between chunks
-  for (int c = 0; c < nch; ++c) {
-    const size_t off = (size_t)(pb[c] - g.pA) * dplane;
-    const size_t cnt = (size_t)(pb[c + 1] - pb[c]) * dplane;
-    VT_CUDA(cudaMemcpyAsync(G->io_stage + off, hsrc + off, cnt * sizeof(double),
-                            cudaMemcpyHostToDevice, G->io_in));
-    VT_CUDA(cudaEventRecord(ev_in[c], G->io_in));
+  for (int c = 0; c < nch && st == VT_OK; ++c) {
+    size_t off, cnt;
+    chunk(c, &off, &cnt);
+    if (stage_in)
+      while (in_done[c].load(std::memory_order_acquire) < T) std::this_thread::yield();
+    cudaError_t e = cudaMemcpyAsync(G->io_stage + off, src + off, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                    G->io_in);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in[c], G->io_in);
+    if (e != cudaSuccess) st = cuda_fail(e, "vt_apply_host H2D");
   }
+  for (auto& w : workers) w.join();
+  workers.clear();
+  if (st != VT_OK) return st;
+  std::vector<int> has_out(nch, 0);
   for (int c = 0; c < nch; ++c) {
     // output planes [pb[c]-1, pb[c+1]-1): they read input planes up to pb[c+1]-1,
     // all inside chunks <= c, so the operator on chunk c starts as soon as its
@@ -403,9 +464,31 @@ vt_status vt_apply_host(vt_grid* G, const double* scale, const double* hu, doubl
       VT_TRY(launch_pack(G, G->io_v, ob, oe, G->io_stage_out + off, s));
       VT_CUDA(cudaEventRecord(ev_k[c], s));
       VT_CUDA(cudaStreamWaitEvent(G->io_out, ev_k[c], 0));
-      VT_CUDA(cudaMemcpyAsync(hdst + off, G->io_stage_out + off, cnt * sizeof(double),
+      VT_CUDA(cudaMemcpyAsync(dst + off, G->io_stage_out + off, cnt * sizeof(double),
                               cudaMemcpyDeviceToHost, G->io_out));
+      if (stage_out) VT_CUDA(cudaEventRecord(ev_in[c], G->io_out));  // (ev_in reused: D2H of c landed)
+      has_out[c] = 1;
     }
+  }
+  if (stage_out) {  // drain the page-locked output chunk by chunk as the D2H copies land
+    std::atomic<int> bad{0};
+    for (int t = 0; t < T; ++t)
+      workers.emplace_back([&, t]() {
+        for (int c = 0; c < nch; ++c) {
+          if (!has_out[c]) continue;
+          const int ob = c == 0 ? pb[0] : pb[c] - 1;
+          const int oe = c == nch - 1 ? pb[nch] : pb[c + 1] - 1;
+          const size_t off = (size_t)(ob - g.pA) * dplane, cnt = (size_t)(oe - ob) * dplane;
+          if (cudaEventSynchronize(ev_in[c]) != cudaSuccess) {
+            bad.store(1);
+            return;
+          }
+          const size_t a = off + cnt * t / T, b = off + cnt * (t + 1) / T;
+          memcpy(hdst + a, G->io_pin_out + a, (b - a) * sizeof(double));
+        }
+      });
+    for (auto& w : workers) w.join();
+    if (bad.load()) return fail(VT_ECUDA, "vt_apply_host: D2H copy failed");
   }
   VT_CUDA(cudaEventRecord(ev_done, G->io_out));
   VT_CUDA(cudaStreamWaitEvent(s, ev_done, 0));

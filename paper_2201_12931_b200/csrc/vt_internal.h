@@ -113,6 +113,7 @@ struct vt_grid {
   // streamed host-to-host apply (vt_apply_host): staging + copy streams
   double *io_stage = nullptr, *io_raw = nullptr, *io_proj = nullptr, *io_v = nullptr;
   double* io_stage_out = nullptr;
+  double *io_pin_in = nullptr, *io_pin_out = nullptr;  // page-locked staging for pageable host arrays
   cudaStream_t io_in = nullptr, io_out = nullptr;
   cudaEvent_t io_ev[33] = {};
 

@@ -188,6 +188,7 @@ def test_streamed_host_apply_matches_device_apply(dims, rng):
         assert lib.vt_apply_host(st.dgrid.handle, ptr(st.scale_dev), u.ctypes.data_as(C.c_void_p),
                                  out.ctypes.data_as(C.c_void_p), nch, stream_ptr()) == 0
         assert np.array_equal(out, ref), nch
-    pinned = vb.apply(st, u)
+    pinned = vb.apply(st, u)  # pageable in (threaded page-locked staging), page-locked out
     assert np.array_equal(pinned, ref)
-    assert torch.cuda.is_available()
+    u_pin = torch.from_numpy(u.copy()).pin_memory().numpy()  # page-locked both ways: direct copies
+    assert np.array_equal(vb.apply(st, u_pin), ref)
