@@ -145,6 +145,19 @@ vt_status vt_hier_create(vt_hier **out, vt_grid *fine, int n_levels, double omeg
 vt_status vt_hier_create_ex(vt_hier **out, vt_grid *fine, int n_levels, double omega, int sweeps,
                             int scheme);
 int vt_hier_scheme(const vt_hier *H);
+/* Fused coarse tail: the V-cycle levels from the first one with at most
+ * `nodes` nodes down to the coarsest direct solve and back up run as ONE
+ * thread-block-cluster kernel (tail.cu) instead of ~7 launches per level.
+ * Applies to hierarchies created afterwards; 0 disables.  Returns the previous
+ * budget (default 0 = off, measured slower than the PDL kernel chain on B200;
+ * or the VT_TAIL_NODES environment variable). */
+long long vt_tail_config(long long nodes);
+/* first level the fused tail covers in a V-cycle entered at level 0; -1: none */
+int vt_hier_tail_level(vt_hier *H);
+/* profiling: enable (1) / disable (0) a 64-slot device record of %globaltimer
+ * after every phase of the fused tail (slot 63: kernel start); host_out (may be
+ * NULL) receives max_slots slots after a device synchronize */
+vt_status vt_tail_trace(int enable, uint64_t *host_out, int max_slots);
 vt_status vt_hier_destroy(vt_hier *H);
 int vt_hier_levels(const vt_hier *H);
 vt_grid *vt_hier_grid(vt_hier *H, int level);

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libvoxb200.so")
 OBJ = os.path.join(HERE, "build")
 SOURCES = ["hex8_apply.cu", "vectors.cu", "multigrid.cu", "design.cu", "runtime.cu", "dist.cu", "dist_design.cu", "galerkin.cu",
-           "peer.cu", "dist_galerkin.cu"]
+           "peer.cu", "dist_galerkin.cu", "tail.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -63,6 +63,9 @@ _SIGS = {
     "vt_hier_destroy": (I, [P]),
     "vt_hier_create_ex": (I, [C.POINTER(P), P, I, D, I, I]),
     "vt_hier_scheme": (I, [P]),
+    "vt_tail_config": (C.c_longlong, [C.c_longlong]),
+    "vt_hier_tail_level": (I, [P]),
+    "vt_tail_trace": (I, [I, P, I]),
     "vt_hier_level_mats": (P, [P, I]),
     "vt_hier_levels": (I, [P]),
     "vt_hier_grid": (P, [P, I]),

@@ -907,7 +907,9 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
     ucur[l] = dst;
     return VT_OK;
   };
-  for (int l = top; l < L - 1; ++l) {
+  // levels >= t run as one fused cluster kernel (tail.cu); t == L: none
+  const int t = hier_tail_start(H, top);
+  for (int l = top; l < L - 1 && l < t; ++l) {
     vt_grid* G = H->lv[l];
     ucur[l] = H->u[l];
     if (H->sweeps >= 1) {
@@ -927,9 +929,15 @@ vt_status hier_vcycle_launch(vt_hier* H, const double* f0, const int* stop, doub
       VT_TRY(launch_restrict(G, H->lv[l + 1], fl[l], H->f[l + 1], stop, -1, -1, s));
     }
   }
-  VT_TRY(launch_coarse_solve(H, fl[L - 1], H->u[L - 1], stop, s));
-  ucur[L - 1] = H->u[L - 1];
-  for (int l = L - 2; l >= top; --l) {
+  if (t < L) {
+    const double* zt = nullptr;
+    VT_TRY(launch_tail(H, t, fl[t], stop, s, &zt));
+    ucur[t] = const_cast<double*>(zt);
+  } else {
+    VT_TRY(launch_coarse_solve(H, fl[L - 1], H->u[L - 1], stop, s));
+    ucur[L - 1] = H->u[L - 1];
+  }
+  for (int l = std::min(L - 2, t - 1); l >= top; --l) {
     vt_grid* G = H->lv[l];
     VT_TRY(launch_prolong_add(H->lv[l + 1], G, ucur[l + 1], ucur[l], stop, s));
     for (int k = 0; k < H->sweeps; ++k) VT_TRY(smooth(l, want_rz && l == 0 && k == H->sweeps - 1));
@@ -1018,6 +1026,10 @@ vt_status vt_hier_create_ex(vt_hier** out, vt_grid* fine, int n_levels, double o
     vt_status st = gal_setup(H);
     if (st != VT_OK) { vt_hier_destroy(H); return st; }
   }
+  {
+    vt_status st = tail_setup(H);
+    if (st != VT_OK) { vt_hier_destroy(H); return st; }
+  }
   *out = H;
   return VT_OK;
 }
@@ -1032,6 +1044,8 @@ vt_status vt_hier_destroy(vt_hier* H) {
     if (l > 0) vt_grid_destroy(H->lv[l]);
   }
   gal_free(H);
+  cudaFree(H->tail_ve);
+  cudaFree(H->tail_bar);
   cudaFree(H->A); cudaFree(H->A0); cudaFree(H->cvec); cudaFree(H->W); cudaFree(H->Kinv); cudaFree(H->k0l); cudaFree(H->status);
   delete H;
   return VT_OK;

@@ -145,6 +145,10 @@ struct vt_hier {
   bool gal_mf = false;              // level 1 applied matrix-free (P^T K0 P)
   bool mats1_fresh = false;         // mats[1] materialized for the current refresh
   double *gfa = nullptr, *gfb = nullptr, *gc1 = nullptr;  // fine x2 / level-1 scratch
+  // fused coarse tail (tail.cu): element-product scratch, first eligible level
+  double* tail_ve = nullptr;
+  void* tail_bar = nullptr;        // grid-barrier words (VT_TAIL_MODE=grid)
+  int tail_first = -1;
 };
 
 namespace vt {
@@ -206,4 +210,9 @@ vt_status launch_gal_vec_epilogue(vt_grid* G, int mode, const double* v, const d
                                   cudaStream_t s);
 vt_status launch_prolong_set(vt_grid* C, vt_grid* F, const double* uc, double* uf, const int* stop,
                              cudaStream_t s);
+// (tail.cu)
+vt_status tail_setup(vt_hier* H);
+int hier_tail_start(vt_hier* H, int top);
+vt_status launch_tail(vt_hier* H, int t, const double* ft, const int* stop, cudaStream_t s,
+                      const double** z_out);
 }  // namespace vt
