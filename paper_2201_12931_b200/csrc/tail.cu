@@ -519,7 +519,8 @@ static long long level_nodes(const vt_grid* G) {
   return (long long)(G->g.nx + 1) * (G->g.ny + 1) * (G->g.nz + 1);
 }
 
-static unsigned long long* g_tail_trace = nullptr;  // device, 64 slots
+static unsigned long long* g_tail_trace_buf = nullptr;  // device, 64 slots
+static unsigned long long* g_tail_trace = nullptr;      // = the buffer while tracing
 
 // VT_TAIL_MODE=grid: one CTA per SM with a software grid barrier instead of a cluster
 static bool tail_grid_mode() {
@@ -674,19 +675,17 @@ long long vt_tail_config(long long nodes) {
 }
 
 vt_status vt_tail_trace(int enable, uint64_t* host_out, int max_slots) {
-  if (enable && !vt::g_tail_trace) {
-    VT_CUDA(cudaMalloc(&vt::g_tail_trace, 64 * sizeof(unsigned long long)));
-    VT_CUDA(cudaMemset(vt::g_tail_trace, 0, 64 * sizeof(unsigned long long)));
+  // the buffer is never freed: a graph captured while tracing keeps its address
+  if (enable && !vt::g_tail_trace_buf) {
+    VT_CUDA(cudaMalloc(&vt::g_tail_trace_buf, 64 * sizeof(unsigned long long)));
+    VT_CUDA(cudaMemset(vt::g_tail_trace_buf, 0, 64 * sizeof(unsigned long long)));
   }
-  if (host_out && vt::g_tail_trace) {
+  if (host_out && vt::g_tail_trace_buf) {
     VT_CUDA(cudaDeviceSynchronize());
-    VT_CUDA(cudaMemcpy(host_out, vt::g_tail_trace, (size_t)std::min(max_slots, 64) * sizeof(uint64_t),
+    VT_CUDA(cudaMemcpy(host_out, vt::g_tail_trace_buf, (size_t)std::min(max_slots, 64) * sizeof(uint64_t),
                        cudaMemcpyDeviceToHost));
   }
-  if (!enable && vt::g_tail_trace) {
-    cudaFree(vt::g_tail_trace);
-    vt::g_tail_trace = nullptr;
-  }
+  vt::g_tail_trace = enable ? vt::g_tail_trace_buf : nullptr;
   return VT_OK;
 }
 
