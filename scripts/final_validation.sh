@@ -16,10 +16,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
     python bench.py --steps 2 --warmup 3 --simp-iters 0 --no-cfg5 --no-cpu > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:hex8_tile_kernel -s 3 -c 1 -f -o $O/${T}_hex8 \
     python scripts/ncu_apply.py > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:hex8_tile_kernel<2, (1|true)" -s 2 -c 1 -f -o $O/${T}_smooth python scripts/pcg_profile.py homogenized > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:hex8_tile_kernel<1, (0|false)" -s 2 -c 1 -f -o $O/${T}_resid python scripts/pcg_profile.py homogenized > /dev/null 2>&1
+# level-0 smoother + r.z (hex8<SMOOTH, dot>) and residual (hex8<RESID>) of the PCG graph
+ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k regex:hex8_tile_kernelILi2ELb1ELb0E -s 2 -c 1 -f -o $O/${T}_smooth python scripts/pcg_profile.py homogenized > $O/${T}_smooth.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k regex:hex8_tile_kernelILi1ELb0ELb0E -s 2 -c 1 -f -o $O/${T}_resid python scripts/pcg_profile.py homogenized > $O/${T}_resid.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${T}_pcg_homog.csv \
     python scripts/pcg_profile.py homogenized > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${T}_pcg_gal.csv \
