@@ -275,7 +275,7 @@ __global__ void gal_node_kernel(Geom g, const uint8_t* __restrict__ mask, const 
       } else if (MODE == 1) {
         val = fx ? 0.0 : __dsub_rn(f[o], v[comp]);
       } else {
-        val = fx ? u[o] : __dadd_rn(u[o], __dmul_rn(omega, __ddiv_rn(__dsub_rn(f[o], v[comp]), d[o])));
+        val = fx ? u[o] : __dadd_rn(u[o], __dmul_rn(omega, ddiv_nr(__dsub_rn(f[o], v[comp]), d[o])));
       }
       out[o] = val;
     }
@@ -310,7 +310,7 @@ __global__ void gal_vec_epilogue_kernel(Geom g, const uint8_t* __restrict__ mask
       else if (MODE == 1)
         val = fx ? 0.0 : __dsub_rn(f[o], v[o]);
       else
-        val = fx ? u[o] : __dadd_rn(u[o], __dmul_rn(omega, __ddiv_rn(__dsub_rn(f[o], v[o]), d[o])));
+        val = fx ? u[o] : __dadd_rn(u[o], __dmul_rn(omega, ddiv_nr(__dsub_rn(f[o], v[o]), d[o])));
       out[o] = val;
     }
   }
@@ -365,7 +365,7 @@ __global__ void gal_jacobi0_kernel(Geom g, const uint8_t* __restrict__ mask, con
 #pragma unroll
     for (int comp = 0; comp < 3; ++comp) {
       const long long o = node * 3 + comp;
-      u[o] = ((m >> comp) & 1u) ? 0.0 : __dmul_rn(omega, __ddiv_rn(f[o], d[o]));
+      u[o] = ((m >> comp) & 1u) ? 0.0 : __dmul_rn(omega, ddiv_nr(f[o], d[o]));
     }
   }
 }

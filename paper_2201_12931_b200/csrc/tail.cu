@@ -96,7 +96,7 @@ __device__ __forceinline__ double jac0(const TailArgs& a, const TailLevel& L, co
     const double w = L.wd[o];
     return w == 0.0 ? 0.0 : __dmul_rn(w, ldcg(f + o));
   }
-  return fx ? 0.0 : __dmul_rn(a.omega, __ddiv_rn(ldcg(f + o), L.d[o]));
+  return fx ? 0.0 : __dmul_rn(a.omega, ddiv_nr(ldcg(f + o), L.d[o]));
 }
 
 // ---- element phase: ve[e] = K_e x_e.  J0: x = jacobi0(f) on the fly.
@@ -232,7 +232,7 @@ __device__ void node_phase(const TailArgs& a, const TailLevel& L, const double* 
         if (a.scheme == 0)  // hex8 SMOOTH: fixed dofs stay 0 (solver-internal vectors)
           out[o] = fx ? 0.0 : fma(__dsub_rn(fo, v[comp]), L.wd[o], xo);
         else                // gal_node_kernel<2>
-          out[o] = fx ? xo : __dadd_rn(xo, __dmul_rn(a.omega, __ddiv_rn(__dsub_rn(fo, v[comp]), L.d[o])));
+          out[o] = fx ? xo : __dadd_rn(xo, __dmul_rn(a.omega, ddiv_nr(__dsub_rn(fo, v[comp]), L.d[o])));
       }
     }
   }
