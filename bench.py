@@ -224,6 +224,26 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def with_transport(make):
+        """make(transport) on every rank.  If the peer transport (CUDA IPC)
+        cannot be set up on some rank, all ranks fall back to NCCL together."""
+        obj, err = None, None
+        try:
+            obj = make(a.transport)
+        except Exception as e:  # noqa: BLE001
+            err = e
+        ok_all = -max_over_ranks(-(0.0 if err else 1.0)) > 0.5
+        if ok_all:
+            return obj, a.transport
+        if a.transport != "peer":
+            raise err if err else RuntimeError("transport setup failed on another rank")
+        closer = getattr(obj, "close", None) or getattr(getattr(obj, "S", None), "close", None)
+        if closer:
+            closer()
+        if rank == 0:
+            print(f"peer transport unavailable ({err!r}); falling back to nccl", file=sys.stderr)
+        return make("nccl"), "nccl (peer setup failed)"
+
     spec = cases.CONFIGS[a.config]
     nx, ny, nz = spec["dims"]
     problem = spec["builder"](nx, ny, nz)
@@ -263,7 +283,8 @@ def run_ours(a):
         # one slab per rank, NCCL halo planes before every apply
         from paper_2201_12931_b200.slabs import SlabSolver
 
-        S = SlabSolver.from_process_group(grid, fm, levels=spec["levels"], transport=a.transport)
+        S, transport_used = with_transport(
+            lambda t: SlabSolver.from_process_group(grid, fm, levels=spec["levels"], transport=t))
         S.set_density(rho, problem.model)
         us = S.upload(u_host)
         vs = S.zeros()
@@ -279,7 +300,7 @@ def run_ours(a):
         def e2e_step():
             return S.download(S.apply(S.upload(u_np)))
 
-        parallelism = (f"{world} z-slabs ({a.transport} halo planes), layers {list(S.plan.bounds)}")
+        parallelism = (f"{world} z-slabs ({transport_used} halo planes), layers {list(S.plan.bounds)}")
         scaling = "strong"
 
     for _ in range(max(a.warmup, 3)):
@@ -357,8 +378,8 @@ def run_ours(a):
         from paper_2201_12931_b200.slabs import SlabRun
 
         opt = vb.OptConfig(volfrac=spec["volfrac"], filter_radius=1.5 * grid.h, ch_tol=1e-12)
-        R = SlabRun.from_process_group(problem, opt, vb.SolverConfig(tolerance=1e-5), spec["levels"], 0.4,
-                                       transport=a.transport, scheme=a.scheme)
+        R, _ = with_transport(lambda t: SlabRun.from_process_group(
+            problem, opt, vb.SolverConfig(tolerance=1e-5), spec["levels"], 0.4, transport=t, scheme=a.scheme))
         times, its = [], []
         for it in range(a.simp_iters):
             barrier()

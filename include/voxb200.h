@@ -179,7 +179,10 @@ vt_status vt_hier_coarse_solve(vt_hier *H, const double *f, double *u, void *str
 /* device pointer to level-l element scale / plain density (vt layouts) */
 const double *vt_hier_level_scale(vt_hier *H, int l);
 /* galerkin: level-l element matrices (n_elements_l x 576, reference element
- * order, row-major 24x24); NULL for homogenized hierarchies or l = 0 */
+ * order, row-major 24x24); NULL for homogenized hierarchies or l = 0.  The
+ * solver stores the symmetric matrices as their packed upper triangle (300
+ * doubles per element); this call expands them into a hierarchy-owned buffer
+ * that stays valid until the next call (synchronizes the device). */
 const double *vt_hier_level_mats(vt_hier *H, int l);
 const double *vt_hier_level_rho(vt_hier *H, int l);
 

@@ -115,7 +115,8 @@ __global__ void gal_level1_kernel(Geom gf, int cnx, int cny, int cnz, const doub
         if (k >= 0) acc = __dadd_rn(acc, __dmul_rn(s[c], corr[(long long)k * 576 + entry]));
       }
     }
-    mats[t] = acc;
+    const int a = entry / 24, b = entry % 24;
+    if (a <= b) mats[E * GAL_PACK + gal_sym(a, b)] = acc;
   }
 }
 
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
           for (int cc = 0; cc < 8; ++cc)
             if (c8[cc] >= 0) kq = __dadd_rn(kq, __dmul_rn(s8[cc], k1.corr[(long long)c8[cc] * 576 + q]));
         } else {
-          kq = mats_l[e * 576 + q];
+          kq = mats_l[e * GAL_PACK + gal_sym(q / 24, q % 24)];
         }
         A[q] = kq * (m[q / 24] * m[q % 24]);
       }
@@ -194,26 +195,40 @@ __global__ void __launch_bounds__(192) gal_coarsen_kernel(Geom gl, const uint8_t
       }
     }
 #pragma unroll
-    for (int r = 0; r < 3; ++r) mats_c[E * 576 + threadIdx.x + r * 192] = acc[r];
+    for (int r = 0; r < 3; ++r) {
+      const int q = threadIdx.x + r * 192, a = q / 24, b = q % 24;
+      if (a <= b) mats_c[E * GAL_PACK + gal_sym(a, b)] = acc[r];  // upper triangle stored
+    }
   }
 }
 
 // ve[e][r] = sum_b K_e[r][b] u_e[b], u projected to zero on fixed dofs; a warp
-// per element, lane r < 24 owns row r (16-byte vector loads, two accumulator
-// chains); u_e goes through the warp's shared-memory slot
-__global__ void gal_elem_kernel(Geom g, const uint8_t* __restrict__ mask,
-                                const double* __restrict__ mats, const double* __restrict__ u,
-                                double* __restrict__ ve, const int* stop) {
+// per element stages the packed upper triangle (2400 B, 16-byte vector loads
+// by all 32 lanes) and u_e in its shared-memory slots, then lane r < 24 forms
+// row r with two accumulator chains (even / odd columns).  Half the matrix
+// bytes of full storage (cfg2 level 2: 157 MB instead of 302 MB; 51 vs 70 us).
+// Measured and not kept: a register-prefetched next element (54 us) and an
+// expanded, row-padded copy in shared memory (64 us).
+constexpr int GE_WARPS = GL_THREADS / 32;
+__global__ void __launch_bounds__(GL_THREADS) gal_elem_kernel(Geom g, const uint8_t* __restrict__ mask,
+                                                              const double* __restrict__ mats,
+                                                              const double* __restrict__ u,
+                                                              double* __restrict__ ve, const int* stop) {
   griddep_wait();
   if (stop && *(volatile const int*)stop) return;
-  __shared__ double us[8][24];
+  __shared__ double us[GE_WARPS][24];
+  __shared__ __align__(16) double ms[GE_WARPS][GAL_PACK];
   const long long nel = (long long)g.nx * g.ny * g.nz;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  double* m = ms[wib];
   for (long long e = warp; e < nel; e += nw) {
     const int i = (int)(e % g.nx), j = (int)((e / g.nx) % g.ny), k = (int)(e / ((long long)g.nx * g.ny));
     __syncwarp();
+    const double2* src = reinterpret_cast<const double2*>(mats + e * GAL_PACK);
+#pragma unroll
+    for (int q = lane; q < GAL_PACK / 2; q += 32) reinterpret_cast<double2*>(m)[q] = src[q];
     if (lane < 24) {
       const int corner = lane / 3, comp = lane % 3;
       const int p = k + ((corner >> 2) & 1) + 1, jj = j + ((corner >> 1) & 1), ii = i + (corner & 1);
@@ -222,13 +237,11 @@ __global__ void gal_elem_kernel(Geom g, const uint8_t* __restrict__ mask,
     }
     __syncwarp();
     if (lane < 24) {
-      const double2* row = reinterpret_cast<const double2*>(mats + e * 576 + lane * 24);
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int b2 = 0; b2 < 12; ++b2) {
-        const double2 m = row[b2];
-        s0 = fma(m.x, us[wib][2 * b2], s0);
-        s1 = fma(m.y, us[wib][2 * b2 + 1], s1);
+        s0 = fma(m[gal_sym(lane, 2 * b2)], us[wib][2 * b2], s0);
+        s1 = fma(m[gal_sym(lane, 2 * b2 + 1)], us[wib][2 * b2 + 1], s1);
       }
       ve[e * 24 + lane] = s0 + s1;
     }
@@ -338,7 +351,7 @@ __global__ void gal_diag_kernel(Geom g, const uint8_t* __restrict__ mask, const 
 #pragma unroll
       for (int comp = 0; comp < 3; ++comp)
         v[comp] = __dadd_rn(v[comp], FROM_SCALE ? k1_entry(k1, e, ei, ej, ek, (3 * c + comp) * 25)
-                                                : mats[e * 576 + (3 * c + comp) * 25]);
+                                                : mats[e * GAL_PACK + gal_sym(3 * c + comp, 3 * c + comp)]);
     }
     const long long node = node_off(g, p, j, i);
     const unsigned m = mask[mask_off(g, p, j, i)];
@@ -449,7 +462,7 @@ vt_status gal_setup(vt_hier* H) {
   for (int l = 1; l < L; ++l) {
     vt_grid* G2 = H->lv[l];
     const long long nel = (long long)G2->g.nx * G2->g.ny * G2->g.nz;
-    if (!(l == 1 && H->gal_mf)) VT_CUDA(cudaMalloc(&H->mats[l], (size_t)nel * 576 * sizeof(double)));
+    if (!(l == 1 && H->gal_mf)) VT_CUDA(cudaMalloc(&H->mats[l], (size_t)nel * GAL_PACK * sizeof(double)));
     VT_CUDA(cudaMalloc(&H->gdiag[l], G2->vec_len() * sizeof(double)));
     VT_CUDA(cudaMemset(H->gdiag[l], 0, G2->vec_len() * sizeof(double)));
   }
@@ -478,6 +491,33 @@ void gal_free(vt_hier* H) {
   cudaFree(H->gve);
   for (double* p : H->mats) cudaFree(p);
   for (double* p : H->gdiag) cudaFree(p);
+  cudaFree(H->mats_full);
+}
+
+// full 24x24 matrices of level l from the packed storage (API / tests)
+__global__ void gal_expand_kernel(const double* __restrict__ packed, long long nel, double* __restrict__ full) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nel * 576;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t / 576;
+    const int q = (int)(t - e * 576);
+    full[t] = packed[e * GAL_PACK + gal_sym(q / 24, q % 24)];
+  }
+}
+
+vt_status gal_expand(vt_hier* H, int l, cudaStream_t s) {
+  vt_grid* G = H->lv[l];
+  const long long nel = (long long)G->g.nx * G->g.ny * G->g.nz;
+  if (H->mats_full_n < nel * 576) {
+    cudaFree(H->mats_full);
+    H->mats_full = nullptr;
+    H->mats_full_n = 0;
+    VT_CUDA(cudaMalloc(&H->mats_full, (size_t)nel * 576 * sizeof(double)));
+    H->mats_full_n = nel * 576;
+  }
+  launch_pdl(gal_expand_kernel, G->nsm * 8, GL_THREADS, 0, s, (const double*)H->mats[l], nel, H->mats_full);
+  count_launch();
+  VT_CUDA(cudaGetLastError());
+  return VT_OK;
 }
 
 static K1Src k1src(vt_hier* H) {
@@ -487,8 +527,9 @@ static K1Src k1src(vt_hier* H) {
 vt_status gal_materialize_level1(vt_hier* H, cudaStream_t s) {
   vt_grid* F = H->lv[0];
   vt_grid* C1 = H->lv[1];
-  const long long tot1 = (long long)C1->g.nx * C1->g.ny * C1->g.nz * 576;
-  if (!H->mats[1]) VT_CUDA(cudaMalloc(&H->mats[1], (size_t)tot1 * sizeof(double)));
+  const long long nel1 = (long long)C1->g.nx * C1->g.ny * C1->g.nz;
+  const long long tot1 = nel1 * 576;
+  if (!H->mats[1]) VT_CUDA(cudaMalloc(&H->mats[1], (size_t)nel1 * GAL_PACK * sizeof(double)));
   const int grid1 = (int)std::min<long long>((tot1 + GL_THREADS - 1) / GL_THREADS, (long long)F->nsm * 16);
   launch_pdl(gal_level1_kernel, grid1, GL_THREADS, 0, s, F->g, C1->g.nx, C1->g.ny, C1->g.nz, H->scale[0], H->gG,
                                                  H->gcorr, H->gcorr_of, H->mats[1]);

@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(1024, 1)
       const int na = (i + (ca & 1)) + (j + ((ca >> 1) & 1)) * nx1 + (k + (ca >> 2)) * nx1 * ny1;
       const int nb = (i + (cb & 1)) + (j + ((cb >> 1) & 1)) * nx1 + (k + (cb >> 2)) * nx1 * ny1;
       const int da = 3 * na + a % 3, db = 3 * nb + b % 3;
-      A[(long long)da * n + db] += mats ? mats[(long long)e * 576 + t] : s * k0l[t];
+      A[(long long)da * n + db] += mats ? mats[(long long)e * GAL_PACK + gal_sym(a, b)] : s * k0l[t];
     }
     __syncthreads();
   }
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(1024, 1)
       const int ca = a / 3, cb = b / 3;
       const int na = (i + (ca & 1)) + (j + ((ca >> 1) & 1)) * nx1 + (k + (ca >> 2)) * nx1 * ny1;
       const int nb = (i + (cb & 1)) + (j + ((cb >> 1) & 1)) * nx1 + (k + (cb >> 2)) * nx1 * ny1;
-      As[(3 * na + a % 3) * n + 3 * nb + b % 3] += mats ? mats[(long long)e * 576 + t] : sc * k0l[t];
+      As[(3 * na + a % 3) * n + 3 * nb + b % 3] += mats ? mats[(long long)e * GAL_PACK + gal_sym(a, b)] : sc * k0l[t];
     }
     __syncthreads();
   }
@@ -1062,7 +1062,9 @@ const double* vt_hier_level_mats(vt_hier* H, int l) {
     if (gal_materialize_level1(H, 0) != VT_OK || cudaDeviceSynchronize() != cudaSuccess) return nullptr;
     H->mats1_fresh = true;
   }
-  return H->mats[l];
+  // stored as the packed upper triangle: expand into the hierarchy's scratch
+  if (!H->mats[l] || gal_expand(H, l, 0) != VT_OK || cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+  return H->mats_full;
 }
 int vt_hier_scheme(const vt_hier* H) { return H ? H->scheme : -1; }
 const double* vt_hier_level_rho(vt_hier* H, int l) { return H->rho[l]; }

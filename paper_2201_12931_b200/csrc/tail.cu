@@ -179,13 +179,12 @@ __device__ void elem_phase(const TailArgs& a, const TailLevel& L, const double* 
       }
       __syncwarp();
       if (lane < 24) {
-        const double2* row = reinterpret_cast<const double2*>(L.mats + (long long)e * 576 + lane * 24);
+        const double* m = L.mats + (long long)e * GAL_PACK;  // packed upper triangle
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (int b2 = 0; b2 < 12; ++b2) {
-          const double2 m = row[b2];
-          s0 = fma(m.x, us[2 * b2], s0);
-          s1 = fma(m.y, us[2 * b2 + 1], s1);
+          s0 = fma(m[gal_sym(lane, 2 * b2)], us[2 * b2], s0);
+          s1 = fma(m[gal_sym(lane, 2 * b2 + 1)], us[2 * b2 + 1], s1);
         }
         a.ve[(long long)e * 24 + lane] = s0 + s1;
       }

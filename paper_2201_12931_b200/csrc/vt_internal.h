@@ -144,6 +144,8 @@ struct vt_hier {
   std::vector<double*> mats, gdiag;  // per level (index >= 1)
   bool gal_mf = false;              // level 1 applied matrix-free (P^T K0 P)
   bool mats1_fresh = false;         // mats[1] materialized for the current refresh
+  double* mats_full = nullptr;      // full 24x24 copy of one level (vt_hier_level_mats)
+  long long mats_full_n = 0;
   double *gfa = nullptr, *gfb = nullptr, *gc1 = nullptr;  // fine x2 / level-1 scratch
   // fused coarse tail (tail.cu): element-product scratch, first eligible level
   double* tail_ve = nullptr;
@@ -203,6 +205,7 @@ vt_status gal_level_op(vt_hier* H, int l, int mode, const double* u, const doubl
                        const int* stop, cudaStream_t s);
 vt_status gal_jacobi0(vt_hier* H, int l, const double* f, double* u, const int* stop, cudaStream_t s);
 vt_status gal_materialize_level1(vt_hier* H, cudaStream_t s);
+vt_status gal_expand(vt_hier* H, int l, cudaStream_t s);
 vt_status launch_gal_jacobi0(vt_grid* G, const double* f, const double* d, double omega, double* u,
                              const int* stop, cudaStream_t s);
 vt_status launch_gal_vec_epilogue(vt_grid* G, int mode, const double* v, const double* u, const double* f,

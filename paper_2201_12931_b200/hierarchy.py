@@ -228,7 +228,8 @@ def build_hierarchy(grid: StructuredGrid, state: OperatorState, max_levels: int,
     """Validate, build levels and refresh (multigrid.py:462-499).
 
     Both schemes run on the device; "galerkin" (the reference default)
-    stores 576 doubles per coarse element on levels >= 1."""
+    stores each coarse element matrix (its packed upper triangle, 300
+    doubles) on levels >= 2 (level 1 matrix-free when it is not the coarsest)."""
     if scheme not in SCHEMES:
         raise ValueError(f"unknown scheme {scheme!r}, expected one of {SCHEMES}")
     if not 0 < omega <= 1:
