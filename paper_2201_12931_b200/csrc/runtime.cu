@@ -554,17 +554,22 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
     if ((st = launch_hex8(G, H8_APPLY, true, scale, G->w_p, nullptr, nullptr, G->w_q, 0.0, P0,
                           &ctl->stop, s)) != VT_OK) break;
     if ((st = launch_pcg_s1(ctl, P0, h8g, s)) != VT_OK) break;
-    // x += alpha p ; r -= alpha q | r = f - K x       [ref: solver.py:131-136]
-    // (MG preconditioner: the same pass writes the V-cycle's first Jacobi sweep)
+    // r -= alpha q | x += alpha p, r = f - K x         [ref: solver.py:131-136]
+    // (MG preconditioner: the same pass writes the V-cycle's first Jacobi sweep).
+    // x += alpha p is deferred to the p update at the end of the iteration (it
+    // reads p there anyway: one 8 B/dof stream fewer), except when the true
+    // residual needs x earlier -- every 50th iteration (mode 0 here) and on a
+    // convergence candidate (mode 2 after S2).
     static const bool fuse_env = !getenv("VT_FUSE_J0") || atoi(getenv("VT_FUSE_J0")) != 0;
     const bool fuse_j0 = fuse_env && precond == 2 && H->lv.size() >= 2 && H->sweeps >= 1 && H->wd[0];
-    if ((st = launch_pcg_update(G, ctl, G->w_x, G->w_p, G->w_r, G->w_q, P1, 1, s,
+    if ((st = launch_pcg_update(G, ctl, nullptr, G->w_p, G->w_r, G->w_q, P1, 1, s,
                                 fuse_j0 ? H->wd[0] : nullptr, fuse_j0 ? H->u[0] : nullptr)) != VT_OK)
       break;
     if ((st = launch_pcg_update(G, ctl, G->w_x, G->w_p, G->w_r, G->w_q, P1, 0, s)) != VT_OK) break;
     if ((st = launch_hex8(G, H8_RESID, true, scale, G->w_x, G->w_x, G->w_f, G->w_r, 0.0, P1,
                           &ctl->skip_true50, s)) != VT_OK) break;
     if ((st = launch_pcg_s2(ctl, P1, dg, h8g, s)) != VT_OK) break;
+    if ((st = launch_pcg_update(G, ctl, G->w_x, G->w_p, G->w_r, G->w_q, P1, 2, s)) != VT_OK) break;
     // convergence candidate: true residual          [ref: solver.py:140-149]
     if ((st = launch_hex8(G, H8_RESID, true, scale, G->w_x, G->w_x, G->w_f, G->w_t, 0.0, P2,
                           &ctl->skip_cand, s)) != VT_OK) break;
@@ -589,7 +594,7 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
     }
     if ((st = launch_pcg_s4(ctl, P3, nrz, precond != 0, s)) != VT_OK) break;
     // p = z + beta p                                  [ref: solver.py:158]
-    if ((st = launch_pcg_xpby(G, ctl, z, G->w_p, s)) != VT_OK) break;
+    if ((st = launch_pcg_xpby(G, ctl, z, G->w_p, s, G->w_x)) != VT_OK) break;
   } while (0);
   cudaGraph_t graph = nullptr;
   cudaError_t ce = cudaStreamEndCapture(s, &graph);

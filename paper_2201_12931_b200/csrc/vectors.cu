@@ -399,21 +399,27 @@ vt_status launch_jacobi0w(vt_grid* G, const double* w, const double* f, double* 
 // ---------------------------------------------------------------- PCG passes
 // x += alpha p ; r -= alpha q ; partial ||r||^2   [ref: solver.py:131-136]
 // (16-byte vector accesses: owned ranges start and end on even indices)
-// With w != nullptr (MG-preconditioned solves) the same pass also writes the
+// mode 1: the recursive update (skipped on k % 50 == 0), plus x += alpha p when
+//         x != nullptr (the slab solver; the single-GPU graph defers x to xpby);
+// mode 0: x += alpha p only, on the k % 50 == 0 iterations (before the true
+//         residual needs it);
+// mode 2: x += alpha p only, for a convergence candidate whose x was deferred.
+// With w != nullptr (MG-preconditioned solves) mode 1 also writes the
 // V-cycle's first damped Jacobi sweep u0 = w r of the updated residual
 // (multigrid.py:387-393), which the V-cycle then skips unless r was replaced
 // by a true residual this iteration (jacobi0w_kernel's ctl test).
 __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict__ x,
                                   const double* __restrict__ p, double* __restrict__ r,
-                                  const double* __restrict__ q, double* partial, int with_r,
+                                  const double* __restrict__ q, double* partial, int mode,
                                   const double* __restrict__ w, double* __restrict__ u0) {
   griddep_wait();
   __shared__ double red[VT_THREADS / 32];
   // The host enqueues iteration k+1 before it sees that iteration k stopped, so
   // every pass of an iteration checks `stop` itself: S1 of a stopped solve
   // returns early and leaves the skip flags of the last live iteration behind.
-  const int skip = with_r ? ctl->skip_rec : ctl->skip_true50;
+  const int skip = mode == 1 ? ctl->skip_rec : (mode == 0 ? ctl->skip_true50 : ctl->skip_xc);
   if (skip || ctl->stop) return;
+  const bool with_r = mode == 1, with_x = x != nullptr;
   const double alpha = ctl->alpha;
   long long b, e;
   owned_range(g, b, e);
@@ -435,8 +441,10 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
     for (int k = 0; k < EW_B; ++k) {
       const long long i = i0 + k * st;
       if (i < n2) {
-        pv[k] = p2[i];
-        xv[k] = x2[i];
+        if (with_x) {
+          pv[k] = p2[i];
+          xv[k] = x2[i];
+        }
         if (with_r) {
           qv[k] = q2[i];
           rv[k] = r2[i];
@@ -448,9 +456,11 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
     for (int k = 0; k < EW_B; ++k) {
       const long long i = i0 + k * st;
       if (i >= n2) break;
-      xv[k].x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
-      xv[k].y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
-      x2[i] = xv[k];
+      if (with_x) {
+        xv[k].x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
+        xv[k].y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
+        x2[i] = xv[k];
+      }
       if (with_r) {
         rv[k].x = __dsub_rn(rv[k].x, __dmul_rn(alpha, qv[k].x));
         rv[k].y = __dsub_rn(rv[k].y, __dmul_rn(alpha, qv[k].y));
@@ -469,32 +479,41 @@ __global__ void pcg_update_kernel(Geom g, const PcgCtl* ctl, double* __restrict_
   }
 }
 
-// p = z + beta p   [ref: solver.py:158]
+// p = z + beta p   [ref: solver.py:158]; with x: first x += alpha p (old p),
+// the update pcg_update deferred, unless x is already current this iteration
 __global__ void pcg_xpby_kernel(Geom g, const PcgCtl* ctl, const double* __restrict__ z,
-                                double* __restrict__ p) {
+                                double* __restrict__ p, double* __restrict__ x) {
   griddep_wait();
   if (ctl->stop) return;
-  const double beta = ctl->beta;
+  const double beta = ctl->beta, alpha = ctl->alpha;
+  const bool with_x = x != nullptr && !ctl->x_done;
   long long b, e;
   owned_range(g, b, e);
   const double2* z2 = reinterpret_cast<const double2*>(z + b);
   double2* p2 = reinterpret_cast<double2*>(p + b);
+  double2* x2 = reinterpret_cast<double2*>(x + b);
   const long long n2 = (e - b) / 2;
   const long long st = (long long)gridDim.x * blockDim.x;
   for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n2; i0 += EW_B * st) {
-    double2 zv[EW_B], pv[EW_B];
+    double2 zv[EW_B], pv[EW_B], xv[EW_B];
 #pragma unroll
     for (int k = 0; k < EW_B; ++k) {
       const long long i = i0 + k * st;
       if (i < n2) {
         zv[k] = z2[i];
         pv[k] = p2[i];
+        if (with_x) xv[k] = x2[i];
       }
     }
 #pragma unroll
     for (int k = 0; k < EW_B; ++k) {
       const long long i = i0 + k * st;
       if (i >= n2) break;
+      if (with_x) {
+        xv[k].x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
+        xv[k].y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
+        x2[i] = xv[k];
+      }
       pv[k].x = __dadd_rn(zv[k].x, __dmul_rn(beta, pv[k].x));
       pv[k].y = __dadd_rn(zv[k].y, __dmul_rn(beta, pv[k].y));
       p2[i] = pv[k];
@@ -558,6 +577,8 @@ __global__ void pcg_s1_kernel(PcgCtl* c, const double* partial, int n) {
   c->skip_true50 = stop || !is50;
   c->skip_cand = 1;
   c->skip_swap = 1;
+  c->skip_xc = 1;
+  c->x_done = is50;  // the mode-0 pass brings x up to date before the true residual
 }
 
 // S2: rel = ||r|| / ||f|| ; candidate convergence [ref: solver.py:137-140]
@@ -574,6 +595,9 @@ __global__ void pcg_s2_kernel(PcgCtl* c, const double* partial, int n_rec, int n
     return;
   }
   c->skip_cand = !(rel <= c->tol);
+  // a candidate's true residual needs the current x: update it now if deferred
+  c->skip_xc = c->skip_cand || c->x_done;
+  if (!c->skip_cand) c->x_done = 1;
 }
 
 // S3: true residual check on a convergence candidate [ref: solver.py:140-149]
@@ -618,8 +642,9 @@ vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p,
   VT_CUDA(cudaGetLastError());
   return VT_OK;
 }
-vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s) {
-  launch_pdl(pcg_xpby_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, ctl, z, p);
+vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s,
+                          double* x) {
+  launch_pdl(pcg_xpby_kernel, G->nsm * 8, VT_THREADS, 0, s, G->g, ctl, z, p, x);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;

@@ -18,7 +18,8 @@ struct PcgCtl {
   int k;
   int err, err_iter;
   int precond_apps;
-  int pad0, pad1;
+  int skip_xc;      // skip the candidate's x update (no candidate, or x already current)
+  int x_done;       // x already holds x + alpha p this iteration (xpby must not add it)
   double err_val;
   double rz, pq, alpha, beta, rel, fnorm, tol, drift;
 };
@@ -26,7 +27,10 @@ struct PcgCtl {
 vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p, double* r,
                             const double* q, double* partial, int with_r, cudaStream_t s,
                             const double* w = nullptr, double* u0 = nullptr);
-vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s);
+// x == nullptr: p = z + beta p only; else also x += alpha p (old p) unless
+// ctl->x_done -- the x update deferred from pcg_update (one stream fewer)
+vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s,
+                          double* x = nullptr);
 vt_status launch_copy(vt_grid* G, const int* skip, const double* src, double* dst,
                       cudaStream_t s);
 vt_status launch_jacobi_precond(vt_grid* G, const int* stop, const double* r, const double* d,
