@@ -574,7 +574,7 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
     if ((st = launch_hex8(G, H8_RESID, true, scale, G->w_x, G->w_x, G->w_f, G->w_t, 0.0, P2,
                           &ctl->skip_cand, s)) != VT_OK) break;
     if ((st = launch_pcg_s3(ctl, P2, h8g, s)) != VT_OK) break;
-    if ((st = launch_copy(G, &ctl->skip_swap, G->w_t, G->w_r, s)) != VT_OK) break;
+    if ((st = launch_copy(G, &ctl->skip_swap, G->w_t, G->w_r, s, G->nsm * 2)) != VT_OK) break;
     // z = M r ; r.z                                   [ref: solver.py:150-151]
     const double* z = G->w_z;
     int nrz = dg;
@@ -595,6 +595,13 @@ static vt_status pcg_capture(vt_grid* G, const double* scale, int precond, vt_hi
     if ((st = launch_pcg_s4(ctl, P3, nrz, precond != 0, s)) != VT_OK) break;
     // p = z + beta p                                  [ref: solver.py:158]
     if ((st = launch_pcg_xpby(G, ctl, z, G->w_p, s, G->w_x)) != VT_OK) break;
+    // measurement hook: VT_PCG_NOOPS extra skipped kernels per iteration (the
+    // in-graph cost of a conditional no-op node; not for production)
+    static const int noops = getenv("VT_PCG_NOOPS") ? atoi(getenv("VT_PCG_NOOPS")) : 0;
+    static const int noop_grid = getenv("VT_PCG_NOOP_GRID") ? atoi(getenv("VT_PCG_NOOP_GRID")) : 0;
+    for (int i = 0; i < noops && st == VT_OK; ++i)
+      st = launch_copy(G, &ctl->skip_swap, G->w_t, G->w_t, s, noop_grid);
+    if (st != VT_OK) break;
   } while (0);
   cudaGraph_t graph = nullptr;
   cudaError_t ce = cudaStreamEndCapture(s, &graph);

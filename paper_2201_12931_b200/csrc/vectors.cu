@@ -388,7 +388,9 @@ vt_status launch_jacobi0w(vt_grid* G, const double* w, const double* f, double* 
                           cudaStream_t s, const PcgCtl* fused) {
   const long long a = (long long)G->g.pA * G->g.nplane, b = (long long)G->g.pB * G->g.nplane;
   const long long n2 = (b - a) / 2;  // nplane is even (rp even)
-  launch_pdl(jacobi0w_kernel, fit_grid(n2, VT_THREADS * EW_B, G->nsm * 8), VT_THREADS, 0, s, n2,
+  // fused: a no-op in most PCG iterations, where a launch's cost grows with its
+  // CTA count (measured in-graph: ~0.8 us at 1 CTA, 2.2 us at 592, 3.7 us at 1184)
+  launch_pdl(jacobi0w_kernel, fit_grid(n2, VT_THREADS * EW_B, G->nsm * (fused ? 2 : 8)), VT_THREADS, 0, s, n2,
              reinterpret_cast<const double2*>(w + a), reinterpret_cast<const double2*>(f + a),
              reinterpret_cast<double2*>(u + a), stop, fused);
   count_launch();
@@ -636,8 +638,10 @@ __global__ void pcg_s4_kernel(PcgCtl* c, const double* partial, int n, int count
 vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p, double* r,
                             const double* q, double* partial, int with_r, cudaStream_t s,
                             const double* w, double* u0) {
-  launch_pdl(pcg_update_kernel, dot_grid(G), VT_THREADS, 0, s, G->g, ctl, x, p, r, q, partial, with_r,
-             w, u0);
+  // modes 0 / 2 (x only) are no-ops in most iterations: a smaller grid costs
+  // less per skipped launch and still streams at full rate when they run
+  launch_pdl(pcg_update_kernel, with_r == 1 ? dot_grid(G) : G->nsm * 2, VT_THREADS, 0, s, G->g, ctl, x, p, r,
+             q, partial, with_r, w, u0);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;
@@ -650,8 +654,9 @@ vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, c
   return VT_OK;
 }
 vt_status launch_copy(vt_grid* G, const int* skip, const double* src, double* dst,
-                      cudaStream_t s) {
-  launch_pdl(copy_kernel, fit_grid((long long)(G->g.pB - G->g.pA) * G->g.nplane, VT_THREADS, G->nsm * 8), VT_THREADS, 0, s, G->g, skip, src, dst);
+                      cudaStream_t s, int grid) {
+  if (grid <= 0) grid = fit_grid((long long)(G->g.pB - G->g.pA) * G->g.nplane, VT_THREADS, G->nsm * 8);
+  launch_pdl(copy_kernel, grid, VT_THREADS, 0, s, G->g, skip, src, dst);
   count_launch();
   VT_CUDA(cudaGetLastError());
   return VT_OK;

@@ -32,7 +32,7 @@ vt_status launch_pcg_update(vt_grid* G, PcgCtl* ctl, double* x, const double* p,
 vt_status launch_pcg_xpby(vt_grid* G, PcgCtl* ctl, const double* z, double* p, cudaStream_t s,
                           double* x = nullptr);
 vt_status launch_copy(vt_grid* G, const int* skip, const double* src, double* dst,
-                      cudaStream_t s);
+                      cudaStream_t s, int grid = 0);
 vt_status launch_jacobi_precond(vt_grid* G, const int* stop, const double* r, const double* d,
                                 double* z, double* partial, cudaStream_t s);
 vt_status launch_pcg_s1(PcgCtl* c, const double* partial, int n, cudaStream_t s);
