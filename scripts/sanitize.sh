@@ -15,14 +15,16 @@ for tool in $tools; do
   if [ $tool = memcheck ]; then
     sets=("tests/test_gpu_operator.py" "tests/test_gpu_solver.py -k \"$SMALL_SOLVER\""
           "tests/test_gpu_galerkin.py -k \"levels or mgcg\"" "tests/test_gpu_slabs.py -k \"$SMALL_SLABS\""
-          "tests/test_gpu_two_material.py -k \"sensitivities or rejects\"")
+          "tests/test_gpu_two_material.py -k \"sensitivities or rejects\""
+          "tests/test_gpu_tail.py -k \"matches_multikernel or coarsest\"")
     extra="--leak-check full"
   else
     # shared-memory hazard / barrier checks: the TMA-ring operator, transfers,
     # V-cycle, coarse solve, PCG graph and the slab exchange at small sizes
     sets=("tests/test_gpu_operator.py -k \"tile_edges or multigrid_matches or vcycle_linear\""
           "tests/test_gpu_solver.py -k \"mgcg_matches or design_kernels\""
-          "tests/test_gpu_galerkin.py -k \"levels\"" "tests/test_gpu_slabs.py -k \"apply_matches or filter_bit\"")
+          "tests/test_gpu_galerkin.py -k \"levels\"" "tests/test_gpu_slabs.py -k \"apply_matches or filter_bit\""
+          "tests/test_gpu_tail.py -k \"matches_multikernel\"")
     extra=""
   fi
   for s in "${sets[@]}"; do
