@@ -33,7 +33,10 @@ def test_galerkin_levels_match_reference(tag):
     for l, lv in enumerate(H.levels):
         if l >= 1:
             want = g[f"{tag}_mats{l}"]
-            assert np.abs(lv.mats - want).max() <= 1e-13 * np.abs(want).max(), l
+            got = lv.mats
+            assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max(), l
+            # stored as packed upper triangles: the expanded copy is exactly symmetric
+            assert np.array_equal(got, got.transpose(0, 2, 1)), l
         assert rel_err(lv.diag, g[f"{tag}_diag{l}"]) <= 1e-13
     for l in range(1, H.n_levels):
         assert rel_err(H.coarse_apply(l, g[f"{tag}_cu{l}"]), g[f"{tag}_cv{l}"]) <= 1e-13
