@@ -453,7 +453,7 @@ vt_status launch_restrict(vt_grid* F, vt_grid* C, const double* rf, double* fc, 
 // slab produces exactly the fine planes it owns.
 constexpr int PJ_MAX = 8, PI_MAX = 42;  // 6 PI <= 256 fine dofs per row: one per thread
 #ifndef VT_PR_B
-#define VT_PR_B 3
+#define VT_PR_B 4
 #endif
 constexpr int PR_B = VT_PR_B;  // coarse rows (2 PR_B fine rows) per batch of read-modify-writes
 
@@ -472,9 +472,7 @@ static ProlongBlk prolong_blocks(const Geom& gc, const Geom& gf, int nsm) {
   b.nJb = (gc.ny + 1 + b.PJ - 1) / b.PJ;
   return b;
 }
-static size_t prolong_smem(const ProlongBlk& b) {
-  return (size_t)2 * (b.PJ + 1) * (b.PI + 1) * 3 * sizeof(double) + (size_t)2 * (2 * b.PJ) * (2 * b.PI);
-}
+static size_t prolong_smem(const ProlongBlk& b) { return (size_t)2 * (b.PJ + 1) * (b.PI + 1) * 3 * sizeof(double); }
 
 template <bool ADD>
 __global__ void __launch_bounds__(MG_THREADS)
@@ -482,11 +480,9 @@ __global__ void __launch_bounds__(MG_THREADS)
                    double* __restrict__ uf, const int* stop, ProlongBlk blk) {
   griddep_wait();
   if (stop && *(volatile const int*)stop) return;
-  extern __shared__ double sc[];  // [kz 2][PJ + 1][3 (PI + 1)], then the masks [cz 2][2 PJ][2 PI]
+  extern __shared__ double sc[];  // [kz 2][PJ + 1][3 (PI + 1)]
   const int fk0 = gf.k0 + gf.pA - 1, fk1 = gf.k0 + gf.pB - 1;
   const int SW = 3 * (blk.PI + 1), SP = (blk.PJ + 1) * SW;
-  const int MW = 2 * blk.PI, MH = 2 * blk.PJ;
-  unsigned char* msk = reinterpret_cast<unsigned char*>(sc + 2 * SP);
   const long long units = (long long)(blk.K1 - blk.K0) * blk.nJb * blk.nIb;
   const long long rowpitch = (long long)gf.rp * 3;
   for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
@@ -499,27 +495,18 @@ __global__ void __launch_bounds__(MG_THREADS)
     // staged coarse rows J0..J0+nJ, nodes I0..I0+nI (clipped to the grid)
     const int sJ = min(nJ + 1, gc.ny + 1 - J0), sw = 3 * min(nI + 1, gc.nx + 1 - I0);
     const int Kp = K + 1 <= gc.nz ? K + 1 : K;
-    // fine planes 2K + cz (owned), rows 2 J0 + ry (<= ny), dofs 3 (2 I0) + e
-    const int fy0 = 2 * J0, fx0 = 2 * I0;
-    const int nfy = min(2 * nJ, gf.ny + 1 - fy0), nfx = min(2 * nI, gf.nx + 1 - fx0);
-    const int czb = (2 * K >= fk0) ? 0 : 1;
-    const int cze = (2 * K + 1 < fk1 && 2 * K + 1 <= gf.nz) ? 2 : 1;
     __syncthreads();
     for (int t = threadIdx.x; t < 2 * sJ * sw; t += blockDim.x) {
       const int r = t / sw, e = t - r * sw;
       const int kz = r / sJ, jj = r - kz * sJ;
       sc[kz * SP + jj * SW + e] = uc[node_off(gc, (kz ? Kp : K) - gc.k0 + 1, J0 + jj, I0) * 3 + e];
     }
-    // the unit's fine fixed-dof masks staged too: the row walk below then has
-    // no dependent global load in front of its stores (the set form has no
-    // other load at all)
-    for (int t = threadIdx.x; t < 2 * nfy * nfx; t += blockDim.x) {
-      const int cz = t / (nfy * nfx), rem = t - cz * (nfy * nfx);
-      const int ry = rem / nfx, ix = rem - ry * nfx;
-      if (cz >= czb && cz < cze)
-        msk[(cz * MH + ry) * MW + ix] = mf[mask_off(gf, 2 * K + cz - gf.k0 + 1, fy0 + ry, fx0 + ix)];
-    }
     __syncthreads();
+    // fine planes 2K + cz (owned), rows 2 J0 + ry (<= ny), dofs 3 (2 I0) + e
+    const int fy0 = 2 * J0, fx0 = 2 * I0;
+    const int nfy = min(2 * nJ, gf.ny + 1 - fy0), nfx = min(2 * nI, gf.nx + 1 - fx0);
+    const int czb = (2 * K >= fk0) ? 0 : 1;
+    const int cze = (2 * K + 1 < fk1 && 2 * K + 1 <= gf.nz) ? 2 : 1;
     for (int e = threadIdx.x; e < 3 * nfx; e += blockDim.x) {
       const int ix = e / 3, comp = e - 3 * ix;
       const bool ox = ix & 1;
@@ -527,7 +514,7 @@ __global__ void __launch_bounds__(MG_THREADS)
       for (int cz = czb; cz < cze; ++cz) {
         const int pf = 2 * K + cz - gf.k0 + 1;
         double* urow = uf + node_off(gf, pf, fy0, fx0) * 3 + e;
-        const unsigned char* mrow = msk + cz * MH * MW + ix;
+        const uint8_t* mrow = mf + mask_off(gf, pf, fy0, fx0 + ix);
         // z pass of coarse row jy at x offsets 0 and +1 (the latter for odd columns)
         auto zrow = [&](int jy, double& z0, double& z1) {
           const double* q = col + jy * SW;
@@ -544,7 +531,7 @@ __global__ void __launch_bounds__(MG_THREADS)
             const int ry = 2 * jy0 + k;
             if (ry >= nfy) break;
             old[k] = ADD ? urow[ry * rowpitch] : 0.0;
-            mk[k] = mrow[ry * MW];
+            mk[k] = mrow[(long long)ry * gf.mp];
           }
 #pragma unroll
           for (int k = 0; k < PR_B; ++k) {
