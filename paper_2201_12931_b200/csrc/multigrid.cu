@@ -27,7 +27,7 @@ constexpr int MG_THREADS = 256;
 #endif
 constexpr int MG_R = VT_MG_R;  // rows in flight per thread in the transfer kernels
 #ifndef VT_MG_CPS
-#define VT_MG_CPS 4
+#define VT_MG_CPS 8
 #endif
 constexpr int MG_CPS = VT_MG_CPS;  // transfer-kernel CTAs per SM (grid cap)
 
