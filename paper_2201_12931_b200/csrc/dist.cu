@@ -96,7 +96,7 @@ static int lvl_k(int k, int l) { return k >> l; }
 
 // ------------------------------------------------------------------ exchanges
 // ghost node planes of level l for one vector per local slab
-vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStream_t s) {
+vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStream_t s, const int* skip) {
   if (D->N == 1) return VT_OK;
   if (!D->remote()) {
     for (int i = 0; i < D->N; ++i) {
@@ -119,7 +119,7 @@ vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStrea
   double* x = v[0];
   if (D->px)
     return peer_halo(D, x + (size_t)g.nplane, x + (size_t)n * g.nplane, x, x + (size_t)(n + 1) * g.nplane,
-                     g.nplane, s);
+                     g.nplane, s, skip);
   auto& A = nccl();
   VT_NCCL(A.GroupStart());
   if (r > 0) {
@@ -345,7 +345,9 @@ static vt_status dist_capture(vt_dist* D, cudaStream_t s) {
       if (st == VT_OK) st = launch_pcg_update(G, ctl, S.x, S.p, S.rr, S.q, G->partial + 4096, 0, s);
     }
     if (st != VT_OK) break;
-    if ((st = halo_nodes(D, 0, vecs(&DSlab::x), s)) != VT_OK) break;
+    // x halo for the true residual; the peer transport skips it (and the
+    // candidate's below) in the iterations that do not need it
+    if ((st = halo_nodes(D, 0, vecs(&DSlab::x), s, &ctl->skip_true50)) != VT_OK) break;
     for (int i = 0; i < NL && st == VT_OK; ++i) {
       DSlab& S = D->sl[i];
       vt_grid* G = S.lv[0];
@@ -356,6 +358,9 @@ static vt_status dist_capture(vt_dist* D, cudaStream_t s) {
     if (st != VT_OK) break;
     if ((st = gather_scal(D, 1, s)) != VT_OK) break;
     if ((st = launch_pcg_s2(ctl, D->scal + D->N, D->N, D->N, s)) != VT_OK) break;
+    // candidate not on a true-residual iteration: its x halo (peer transport;
+    // the others exchanged x unconditionally above)
+    if (D->px && (st = halo_nodes(D, 0, vecs(&DSlab::x), s, &ctl->skip_xc)) != VT_OK) break;
     // convergence candidate: true residual          [ref: solver.py:140-149]
     for (int i = 0; i < NL && st == VT_OK; ++i) {
       DSlab& S = D->sl[i];

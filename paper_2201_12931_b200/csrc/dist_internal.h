@@ -55,6 +55,8 @@ struct PeerOps {
   long long qoff[XP_MAXOPS], qn[XP_MAXOPS];
   double* qdst[XP_MAXOPS];
   int wpeer[XP_MAXOPS];                       // ranks synchronised with (symmetric)
+  const int* skip = nullptr;                  // device word: nonzero = skip the whole exchange
+                                              // (every rank reads the same value)
   void pack(const double* src, long long off, long long n) {
     psrc[npack] = src; poff[npack] = off; pn[npack] = n; ++npack;
   }
@@ -77,6 +79,7 @@ struct XArgs {
   unsigned long long* ctr;    // local: [0] epoch
   unsigned* cnt;              // local: [0] packers, [1] pullers
   int* err;                   // mapped host word
+  const int* skip;            // see PeerOps::skip
   unsigned long long timeout_ns;
 };
 
@@ -141,7 +144,10 @@ namespace vt {
                                       " at " #call);                                         \
   } while (0)
 
-vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStream_t s);
+// skip (peer transport only): device word read by the exchange kernel; nonzero
+// on every rank = no exchange (the other transports always exchange)
+vt_status halo_nodes(vt_dist* D, int l, const std::vector<double*>& v, cudaStream_t s,
+                     const int* skip = nullptr);
 vt_status halo_elems(vt_dist* D, int l, const std::vector<double*>& e, cudaStream_t s);
 vt_status gather_scal(vt_dist* D, int slot, cudaStream_t s);
 vt_status slab_sum(vt_dist* D, int i, const double* partial, int n, int n50, int slot,
@@ -161,5 +167,5 @@ PeerOps peer_all_but_self(vt_dist* D);
 // neighbour halo: send `down` (n doubles) to rank-1 and `up` to rank+1, receive
 // rank-1's `up` into below and rank+1's `down` into above
 vt_status peer_halo(vt_dist* D, const double* down, const double* up, double* below, double* above,
-                    long long n, cudaStream_t s);
+                    long long n, cudaStream_t s, const int* skip = nullptr);
 }  // namespace vt

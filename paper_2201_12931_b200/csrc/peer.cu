@@ -68,6 +68,8 @@ __device__ bool wait_flags(unsigned long long* const* fl, int nw, int which, uns
 
 __global__ void __launch_bounds__(XP_THREADS)
     xchg_kernel(XArgs a) {
+  // a conditional exchange (same flag value on every rank): no epoch is used
+  if (a.skip && *(volatile const int*)a.skip) return;
   __shared__ unsigned long long e;
   __shared__ int ok;
   if (threadIdx.x == 0) {
@@ -185,6 +187,7 @@ vt_status peer_exchange(vt_dist* D, const PeerOps& ops, cudaStream_t s) {
   a.cnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(P->local) + 16);
   a.err = P->err_dev;
   a.timeout_ns = P->timeout_ns;
+  a.skip = ops.skip;
   long long total = 0;
   a.npack = ops.npack;
   for (int i = 0; i < ops.npack; ++i) {
@@ -273,7 +276,7 @@ vt_status vt_dist_peer_open(vt_dist* D, const uint8_t* handles, int nbytes) {
 namespace vt {
 
 vt_status peer_halo(vt_dist* D, const double* down, const double* up, double* below, double* above,
-                    long long n, cudaStream_t s) {
+                    long long n, cudaStream_t s, const int* skip) {
   PeerXport* P = D->px;
   if ((size_t)n > P->half) return fail(VT_EINVAL, "halo exceeds the peer staging area");
   const int r = D->sl[0].rank;
@@ -288,6 +291,7 @@ vt_status peer_halo(vt_dist* D, const double* down, const double* up, double* be
     o.pull(r + 1, 0, above, n);                  // rank+1's first planes
     o.wait(r + 1);
   }
+  o.skip = skip;
   return peer_exchange(D, o, s);
 }
 

@@ -42,7 +42,7 @@ def _summary(res):
             res.densities.values.copy(), np.asarray(res.displacement).copy())
 
 
-def _worker(rank, world, port, dims, gravity, iters, q, scheme="homogenized"):
+def _worker(rank, world, port, dims, gravity, iters, q, scheme="homogenized", tol=1e-8):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     os.environ.setdefault("VT_PEER_TIMEOUT_S", "120")
     import torch.distributed as dist
@@ -56,7 +56,7 @@ def _worker(rank, world, port, dims, gravity, iters, q, scheme="homogenized"):
     try:
         prob = _problem(vb, O, *dims, gravity=gravity)
         opt = vb.OptConfig(volfrac=0.12, filter_radius=1.5 * prob.grid.h, max_iterations=iters, ch_tol=1e-12)
-        cfg = vb.SolverConfig(tolerance=1e-8, max_iterations=300)
+        cfg = vb.SolverConfig(tolerance=tol, max_iterations=300)
         l0 = vb.launch_count()
         mp_res = _summary(run_slabs(prob, opt, cfg, max_levels=3, group=dist.group.WORLD, transport="peer",
                                     scheme=scheme))
@@ -73,13 +73,13 @@ def _worker(rank, world, port, dims, gravity, iters, q, scheme="homogenized"):
         dist.destroy_process_group()
 
 
-def _run(dims, gravity=None, iters=3, world=2, scheme="homogenized"):
+def _run(dims, gravity=None, iters=3, world=2, scheme="homogenized", tol=1e-8):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, gravity, iters, q, scheme))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, gravity, iters, q, scheme, tol))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -111,6 +111,17 @@ def test_two_process_run_with_self_weight():
 def test_two_process_galerkin_run_bit_identical_to_in_process_slabs():
     """The reference's default scheme with one slab per process."""
     _, (recs, rho, u), (rrecs, rrho, ru), _ = _run((16, 8, 16), scheme="galerkin", iters=2)
+    assert recs == rrecs
+    assert np.array_equal(rho, rrho)
+    assert np.array_equal(u, ru)
+
+
+def test_two_process_true_residual_iterations():
+    """Solves long enough to pass the every-50-iterations true residual: the
+    peer transport exchanges x's halo only in those iterations and for
+    convergence candidates (skip words read by the exchange kernel)."""
+    _, (recs, rho, u), (rrecs, rrho, ru), _ = _run((16, 8, 16), iters=8, tol=1e-12)
+    assert max(r[4] for r in recs) > 50, recs  # CG iterations of the longest solve
     assert recs == rrecs
     assert np.array_equal(rho, rrho)
     assert np.array_equal(u, ru)
