@@ -364,14 +364,14 @@ def run_ours(a):
     # run() (RunRecord.wall_s, as the reference times it: optimize.py:441)
     if a.simp_iters > 0 and not slabs:
         del state, u, v
-        solve = full_run(vb, problem, spec, "homogenized", a.simp_iters)
-        solve_galerkin = full_run(vb, problem, spec, "galerkin", a.simp_iters)
+        solve = _guard(lambda: full_run(vb, problem, spec, "homogenized", a.simp_iters))
+        solve_galerkin = _guard(lambda: full_run(vb, problem, spec, "galerkin", a.simp_iters))
         solve_galerkin["note"] = ("the same run with scheme='galerkin' (the reference default; refresh "
                                   "builds the coarse element matrices, level 1 matrix-free)")
         # BASELINE cfg1 (the CPU-runnable oracle config) end to end on the GPU, for the
         # like-for-like CPU comparison in cpu_baseline.solve
         c1 = cases.CONFIGS["cfg1"]
-        extra["cfg1_run"] = full_run(vb, c1["builder"](*c1["dims"]), c1, "homogenized", 40)
+        extra["cfg1_run"] = _guard(lambda: full_run(vb, c1["builder"](*c1["dims"]), c1, "homogenized", 40))
     elif a.simp_iters > 0:
         # the same design iterations on the slabs (SlabRun: refresh + slab MGPCG, then the
         # distributed sensitivities / filter / OC), time of the solve part, max over ranks
@@ -432,17 +432,30 @@ def run_ours(a):
     if solve_galerkin is not None:
         res["solve_galerkin"] = solve_galerkin
     res.update(extra)
+    # secondary sections: a failure is recorded in the line instead of losing it
     if not slabs and not a.no_cfg5 and a.config == "cfg2":
-        res["cfg5_single_gpu"] = cfg5_section(vb, a.cfg5_iters)
+        res["cfg5_single_gpu"] = _guard(lambda: cfg5_section(vb, a.cfg5_iters))
     if rank == 0 and world == 1 and not a.no_cpu:
-        res["cpu_baseline"] = cpu_baseline(a.config, reps=2)
+        res["cpu_baseline"] = _guard(lambda: cpu_baseline(a.config, reps=2))
         cg = (solve or {}).get("cg_mean")
-        res["cpu_baseline"]["solve"] = cpu_solve_baseline(a.config, cg)
+        if "error" not in res["cpu_baseline"]:
+            res["cpu_baseline"]["solve"] = _guard(lambda: cpu_solve_baseline(a.config, cg))
     if slabs:
         S.close()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(res))
+
+
+def _guard(fn):
+    """Run one secondary bench section; an exception becomes {"error": ...}."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        traceback.print_exc(file=sys.stderr)
+        return {"error": repr(e)[:300]}
 
 
 def _run_summary(times, its):
