@@ -9,7 +9,10 @@
 namespace vt {
 
 constexpr int VT_THREADS = 256;
-constexpr int EW_B = 4;  // elements in flight per thread in the streaming kernels
+#ifndef VT_EW_B
+#define VT_EW_B 2
+#endif
+constexpr int EW_B = VT_EW_B;  // elements in flight per thread in the streaming kernels
 
 int dot_grid(vt_grid* G) { return G->nsm * 4; }
 
