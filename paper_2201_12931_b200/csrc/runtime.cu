@@ -134,6 +134,20 @@ const CUtensorMap* vec_map(vt_grid* G, const void* ptr) {
   return &(G->vec_maps[ptr] = m);
 }
 
+// rhs vector of the residual / smoother: the same layout, box of the owned
+// node rows only (TY - 1 rows)
+const CUtensorMap* fvec_map(vt_grid* G, const void* ptr) {
+  auto it = G->fvec_maps.find(ptr);
+  if (it != G->fvec_maps.end()) return &it->second;
+  CUtensorMap m;
+  const Geom& g = G->g;
+  if (!encode3d(&m, ptr, 3ull * (g.nx + 1), g.ny + 1, g.P, 24ull * g.rp,
+                24ull * g.rp * (g.ny + 1), 100, H8_TY - 1))
+    return nullptr;
+  if (G->fvec_maps.size() > 256) G->fvec_maps.clear();
+  return &(G->fvec_maps[ptr] = m);
+}
+
 // fine-level node vector seen as (dofs of a row, rows, planes) with a
 // (box_x dofs, box_y rows, 1 plane) box: the staged blocks of the restriction
 const CUtensorMap* xfer_map(vt_grid* G, const void* ptr, unsigned box_x, unsigned box_y) {

@@ -101,6 +101,7 @@ struct vt_grid {
   std::map<const void*, CUtensorMap> vec_maps;   // node-vector TMA descriptors
   std::map<const void*, CUtensorMap> elem_maps;  // element-field TMA descriptors
   std::map<const void*, CUtensorMap> xfer_maps;  // node-vector descriptors of the TMA restriction
+  std::map<const void*, CUtensorMap> fvec_maps;  // rhs tiles of the residual / smoother (owned rows)
   // PCG workspace (lazily allocated)
   double *w_x = nullptr, *w_f = nullptr, *w_r = nullptr, *w_p = nullptr, *w_q = nullptr,
          *w_z = nullptr, *w_t = nullptr, *w_d = nullptr;
@@ -159,6 +160,7 @@ vt_status hier_refresh_levels(vt_hier* H, double p, double kmin, double E, cudaS
 const CUtensorMap* vec_map(vt_grid* G, const void* ptr);
 const CUtensorMap* elem_map(vt_grid* G, const void* ptr);
 const CUtensorMap* xfer_map(vt_grid* G, const void* ptr, unsigned box_x, unsigned box_y);
+const CUtensorMap* fvec_map(vt_grid* G, const void* ptr);
 
 // kernel launchers (hex8_apply.cu)
 Hex8Launch hex8_plan(const Geom& g, int nsm);
